@@ -1,0 +1,96 @@
+"""The CPU oracle (oracle/simba_oracle.c) against golden vectors produced by the
+unmodified reference (tests/golden/make_golden.py).  This pins the oracle that
+every GPU parity test then trusts."""
+
+import hashlib
+
+import pytest
+
+import oracle as O
+from conftest import load_golden
+
+
+def test_tables_match_reference():
+    d = load_golden("tables")
+    for t in d["tables"]:
+        ot = O.OracleTable(t["k"], t["max_size"])
+        assert ot.rows() == t["rows"], t["k"]
+        assert [ot.cumulative(s) for s in range(1, t["max_size"] + 1)] == t["cumulative"][1:]
+
+
+def test_capacity_error_matches_reference():
+    cap = load_golden("tables")["capacity_error"]
+    with pytest.raises(O.CapacityError) as exc:
+        O.OracleTable(cap["k"], cap["max_size"])
+    assert (exc.value.s, exc.value.op) == (cap["s"], cap["op"])
+
+
+def test_decode_digests_every_rank():
+    for g in load_golden("decode")["digests"]:
+        t = O.OracleTable(g["k"], g["s"])
+        h = hashlib.sha256()
+        for n in range(g["total"]):
+            toks = O.decode(t, n, g["s"])
+            h.update(bytes((x & 0xFF) for x in toks))
+            if g["tokens"] is not None:
+                assert list(toks) == g["tokens"][n]
+        assert h.hexdigest() == g["sha256"], (g["k"], g["s"])
+
+
+def test_decode_samples_large_sizes():
+    tables = {}
+    for smp in load_golden("decode")["samples"]:
+        k = smp["k"]
+        if k not in tables:
+            tables[k] = O.OracleTable(k, 24 if k == 1 else 16)
+        assert list(O.decode(tables[k], smp["rank"], smp["s"])) == smp["tokens"]
+
+
+def test_eval_vectors():
+    for e in load_golden("eval"):
+        assert O.eval_tokens(e["tokens"], e["inputs"], e["w"]) == e["value"]
+
+
+def _pairs(spec):
+    return [(tuple(i), o) for i, o in spec["pairs"]]
+
+
+def test_search_outcomes_match_reference():
+    for r in load_golden("search"):
+        sp = r["spec"]
+        t = O.OracleTable(sp["k"], r["size_bound"])
+        o = O.synthesize(t, sp["k"], sp["w"], _pairs(sp), r["size_bound"])
+        assert (o["status"], o["size"], o["rank"], o["tokens"], o["per_size"]) == (
+            r["status"], r["size"], r["rank"], r["tokens"], r["per_size"]), r["name"]
+
+
+def test_exhaustive_counts_match_reference():
+    for r in load_golden("counts"):
+        sp = r["spec"]
+        t = O.OracleTable(sp["k"], r["size_bound"])
+        for s, c, first in r["per_size"]:
+            _, cnt, best, _ = O.scan_range(t, sp["k"], sp["w"], _pairs(sp), s, 0, t.total(s),
+                                           0, t.total(s), threads=O.cpu_count())
+            assert (cnt, best) == (c, first), (r["name"], s)
+
+
+def test_rank_windows_match_reference():
+    for r in load_golden("windows"):
+        sp = r["spec"]
+        t = O.OracleTable(sp["k"], r["size_bound"])
+        _, cnt, best, _ = O.scan_range(t, sp["k"], sp["w"], _pairs(sp), r["size"], 0,
+                                       t.total(r["size"]), r["lo"], r["hi"], threads=O.cpu_count())
+        assert (cnt, best) == (r["count"], r["first"]), r["name"]
+
+
+def test_shuffled_scan_same_min_and_count():
+    # codec.py:210-236 / engine.py:145: the permutation changes only the order.
+    r = load_golden("counts")[-1]
+    sp = r["spec"]
+    t = O.OracleTable(sp["k"], r["size_bound"])
+    s = 7
+    off = t.operator_offset(s, 5)
+    tot = t.entry(s, 5)
+    a = O.scan_range(t, sp["k"], sp["w"], _pairs(sp), s, off, tot, 0, tot)
+    b = O.scan_range(t, sp["k"], sp["w"], _pairs(sp), s, off, tot, 0, tot, shuffled=True)
+    assert a[1] == b[1] and a[2] == b[2]
