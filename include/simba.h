@@ -1,0 +1,167 @@
+/*
+ * simba.h -- C ABI of the B200-native SIMBA hot path (libsimba.so).
+ *
+ * The reference (arxiv 2605.08243, package `mbasynth`, pure Python) has no FFI.
+ * Its backend seam is the data-parallel map over a rank range
+ * ("a pluggable data-parallel map over an index range whose body
+ * is pure"), i.e. `engine._scan_range` (engine.py:128-156) dispatched by
+ * `engine.synthesize` (engine.py:240-243).  Each entry point below names the
+ * reference function it replaces.  INTEGRATION.md shows the ctypes binding a
+ * maintainer adds to engine.py to route the reference through this library.
+ *
+ * Conventions: plain pointers and sizes, no exceptions across the ABI, every
+ * function returns a SIMBA_* status code; `simba_last_error()` gives the
+ * message of the last failure on the calling thread.  All calls are
+ * synchronous.  There is no CPU fallback: on a host without a CUDA device the
+ * context constructor fails with SIMBA_ECUDA.
+ */
+#ifndef SIMBA_H
+#define SIMBA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SIMBA_OK 0
+#define SIMBA_EINVAL 1      /* bad argument (ValueError in the reference) */
+#define SIMBA_ERANGE 2      /* rank/size outside the table, or a count >= 2^64 */
+#define SIMBA_ECAPACITY 3   /* counting.CountCapacityError (counting.py:35-43) */
+#define SIMBA_ECUDA 4       /* CUDA runtime failure / no device */
+#define SIMBA_ENOMEM 5
+
+/* Largest expression size the device path supports (token buffer length). */
+#define SIMBA_MAX_SIZE 24
+/* Largest table extent simba_table_build accepts (128-bit host arithmetic). */
+#define SIMBA_TABLE_MAX 64
+
+#define SIMBA_MODE_SEARCH 0 /* minimum satisfying rank, early exit above it */
+#define SIMBA_MODE_COUNT 1  /* exhaustive satisfying-candidate count */
+
+#define SIMBA_STATUS_FOUND 0     /* engine.Status.FOUND     (engine.py:31-37) */
+#define SIMBA_STATUS_NOT_FOUND 1 /* engine.Status.NOT_FOUND */
+#define SIMBA_STATUS_TIMED_OUT 2 /* engine.Status.TIMED_OUT */
+
+#define SIMBA_NO_RANK UINT64_MAX
+
+/* ---------------------------------------------------------------------- */
+/* Tables                                                                  */
+/* ---------------------------------------------------------------------- */
+
+/* counting.build(k, max_size) (counting.py:88-128).  Fills rows[s*9 + op]
+ * (s = 0..max_size, op = 0..8, slot 8 = total) and cumulative[s] as 128-bit
+ * values split into lo/hi words.  Returns SIMBA_ECAPACITY and sets
+ * (*err_s, *err_op) at the first entry above 2^128-1, exactly like
+ * CountCapacityError (counting.py:115-117). */
+int simba_table_build(int k, int max_size, uint64_t *rows_lo, uint64_t *rows_hi,
+                      uint64_t *cum_lo, uint64_t *cum_hi, int *err_s, int *err_op);
+
+/* ---------------------------------------------------------------------- */
+/* Context: one Specification bound to one device                          */
+/* ---------------------------------------------------------------------- */
+
+typedef struct simba_ctx simba_ctx;
+
+typedef struct {
+    int device;          /* CUDA ordinal (default 0) */
+    int r0;              /* super-leaf size cutoff; 0 = auto */
+    int table_examples;  /* examples with value tables (1, 2 or 4); 0 = auto */
+    int block_threads;   /* 0 = auto (256) */
+    int blocks_per_sm;   /* 0 = occupancy calculator */
+    int kernel;          /* 0 = unit kernel (default), 1 = per-rank direct kernel */
+} simba_options;
+
+/* Binds a Specification (engine.py:40-78; inputs row-major [n][k], outputs
+ * [n]) and the count table for sizes 1..max_size to a device: stages the
+ * tables, the examples and the per-spec super-leaf value tables in device
+ * memory.  Validation matches Specification.__post_init__ (engine.py:52-67):
+ * k >= 1, 1 <= w <= 64, n >= 1, values < 2^w, pairwise-distinct inputs ->
+ * SIMBA_EINVAL.  T[s][8] >= 2^64 for some s <= max_size -> SIMBA_ERANGE.
+ * opt may be NULL (defaults). */
+int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t *outputs,
+                     int max_size, const simba_options *opt, simba_ctx **out);
+void simba_ctx_destroy(simba_ctx *ctx);
+
+typedef struct {
+    uint64_t visited;    /* candidates whose evaluation completed */
+    uint64_t count;      /* satisfying candidates (exact in COUNT mode) */
+    uint64_t best_rank;  /* minimum satisfying in-size rank, SIMBA_NO_RANK if none */
+    int32_t found;
+    int32_t completed;   /* 0 when a time budget stopped the scan early */
+    int32_t size;
+    int32_t tokens[SIMBA_MAX_SIZE]; /* RPN tokens of best_rank (expr.py:66-85) */
+    double kernel_ms;    /* device time of the scan launch (CUDA events) */
+    uint64_t launches;   /* kernels launched for this call */
+    uint64_t units;      /* units decoded by the unit kernel */
+    uint64_t rank_units; /* units that took the per-rank path */
+} simba_result;
+
+/* engine._scan_range(ctx, size, offset, block_total, start, stop, shuffled)
+ * (engine.py:128-156): decode-evaluate-discard local indices [start, stop) of
+ * the operator block starting at in-size rank `offset` with `block_total`
+ * candidates; local index i maps to rank offset + i, or to
+ * offset + (i * 2246822507 mod block_total) when shuffled (engine.py:145,
+ * codec.py:29).  Returns visited = stop - start and the minimum satisfying
+ * rank with its tokens, like the reference's (visited, best_rank, best_tokens). */
+int simba_scan_range(simba_ctx *ctx, int size, uint64_t offset, uint64_t block_total,
+                     uint64_t start, uint64_t stop, int shuffled, simba_result *out);
+
+/* General range request: in-size ranks [lo, hi) at `size`, cut into chunks
+ * of `chunk` ranks (0 = auto); this caller processes chunks c with
+ * c % nshards == shard (round-robin super-chunks for multi-GPU sharding,
+ * SURVEY.md 8(e)).  SEARCH mode stops claiming chunks above the best hit
+ * (and above `stop_above`, a bound learnt from other shards); COUNT mode
+ * visits every rank.  time_budget_s < 0 disables the budget, which is
+ * polled between chunks only and never masks a recorded hit
+ * (engine.py:251-258). */
+typedef struct {
+    int size;
+    int mode;
+    uint64_t lo, hi;
+    uint64_t chunk;
+    uint64_t shard, nshards;
+    uint64_t stop_above;
+    double time_budget_s;
+} simba_range;
+
+int simba_run(simba_ctx *ctx, const simba_range *req, simba_result *out);
+
+/* engine.synthesize (engine.py:190-276), Algorithm 1 on the device: sizes
+ * 1..size_bound ascending, each size level scanned in rank order (operator
+ * blocks are contiguous rank ranges in slot order, engine.py:175-187) with
+ * early exit above the best hit; result = (minimum size with a hit, minimum
+ * in-size rank at that size), identical in local and shuffled mode. */
+typedef struct {
+    int32_t status;      /* SIMBA_STATUS_* */
+    int32_t size;
+    uint64_t rank;
+    int32_t tokens[SIMBA_MAX_SIZE];
+    int32_t nsizes;      /* entries in the per-size stats (SizeStats) */
+    uint64_t visited[SIMBA_MAX_SIZE];
+    double millis[SIMBA_MAX_SIZE];
+    double kernel_ms;
+    uint64_t launches;
+} simba_outcome;
+
+int simba_synthesize(simba_ctx *ctx, int size_bound, int shuffled, double time_budget_s,
+                     simba_outcome *out);
+
+/* codec.decode(rank, size, table) (codec.py:136-144) on the device. */
+int simba_decode(simba_ctx *ctx, uint64_t rank, int size, int32_t *tokens);
+
+/* Effective configuration of a context (for reports): r0, table examples,
+ * word bytes, grid blocks, block threads, shared-memory bytes per block. */
+int simba_ctx_info(simba_ctx *ctx, int *r0, int *table_examples, int *word_bytes, int *grid_blocks,
+                   int *block_threads, int *smem_bytes);
+
+const char *simba_last_error(void);
+int simba_device_count(void);
+/* Kernels this library has launched in this process. */
+uint64_t simba_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SIMBA_H */

@@ -1,0 +1,144 @@
+"""ctypes binding of libsimba.so (include/simba.h).
+
+The library is built in-tree (``python __graft_entry__.py`` or
+``python -m paper_2605_08243_b200._build``).  There is no CPU fallback: if the
+library is missing this module raises ImportError, and if no CUDA device is
+present every device call fails with DeviceError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "_lib" / "libsimba.so"
+
+OK, EINVAL, ERANGE, ECAPACITY, ECUDA, ENOMEM = 0, 1, 2, 3, 4, 5
+MAX_SIZE = 24
+TABLE_MAX = 64
+MODE_SEARCH, MODE_COUNT = 0, 1
+STATUS_FOUND, STATUS_NOT_FOUND, STATUS_TIMED_OUT = 0, 1, 2
+NO_RANK = (1 << 64) - 1
+
+
+class Options(C.Structure):
+    _fields_ = [
+        ("device", C.c_int),
+        ("r0", C.c_int),
+        ("table_examples", C.c_int),
+        ("block_threads", C.c_int),
+        ("blocks_per_sm", C.c_int),
+        ("kernel", C.c_int),
+    ]
+
+
+class Result(C.Structure):
+    _fields_ = [
+        ("visited", C.c_uint64),
+        ("count", C.c_uint64),
+        ("best_rank", C.c_uint64),
+        ("found", C.c_int32),
+        ("completed", C.c_int32),
+        ("size", C.c_int32),
+        ("tokens", C.c_int32 * MAX_SIZE),
+        ("kernel_ms", C.c_double),
+        ("launches", C.c_uint64),
+        ("units", C.c_uint64),
+        ("rank_units", C.c_uint64),
+    ]
+
+
+class Range(C.Structure):
+    _fields_ = [
+        ("size", C.c_int),
+        ("mode", C.c_int),
+        ("lo", C.c_uint64),
+        ("hi", C.c_uint64),
+        ("chunk", C.c_uint64),
+        ("shard", C.c_uint64),
+        ("nshards", C.c_uint64),
+        ("stop_above", C.c_uint64),
+        ("time_budget_s", C.c_double),
+    ]
+
+
+class Outcome(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32),
+        ("size", C.c_int32),
+        ("rank", C.c_uint64),
+        ("tokens", C.c_int32 * MAX_SIZE),
+        ("nsizes", C.c_int32),
+        ("visited", C.c_uint64 * MAX_SIZE),
+        ("millis", C.c_double * MAX_SIZE),
+        ("kernel_ms", C.c_double),
+        ("launches", C.c_uint64),
+    ]
+
+
+# every symbol include/simba.h declares, with its ctypes signature
+SIGNATURES = {
+    "simba_table_build": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                    C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                    C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "simba_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                   C.c_int, C.POINTER(Options), C.POINTER(C.c_void_p)]),
+    "simba_ctx_destroy": (None, [C.c_void_p]),
+    "simba_scan_range": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                   C.c_int, C.POINTER(Result)]),
+    "simba_run": (C.c_int, [C.c_void_p, C.POINTER(Range), C.POINTER(Result)]),
+    "simba_synthesize": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_double, C.POINTER(Outcome)]),
+    "simba_decode": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
+    "simba_ctx_info": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int)] * 6),
+    "simba_last_error": (C.c_char_p, []),
+    "simba_device_count": (C.c_int, []),
+    "simba_launch_count": (C.c_uint64, []),
+}
+
+
+def _load():
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python __graft_entry__.py` (nvcc, sm_100a). "
+            "The SIMBA device path has no CPU fallback.")
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or missing device (SIMBA_ECUDA)."""
+
+
+def last_error() -> str:
+    msg = lib.simba_last_error()
+    return msg.decode() if msg else ""
+
+
+def check_rc(rc: int, what: str = "") -> None:
+    """Map a SIMBA_* status code to the exception the reference raises."""
+    if rc == OK:
+        return
+    msg = last_error() or what
+    if rc in (EINVAL, ERANGE):
+        raise ValueError(msg)
+    if rc == ECAPACITY:
+        raise OverflowError(msg)
+    if rc == ENOMEM:
+        raise MemoryError(msg)
+    raise DeviceError(msg)
+
+
+def device_count() -> int:
+    return lib.simba_device_count()
+
+
+def launch_count() -> int:
+    return lib.simba_launch_count()

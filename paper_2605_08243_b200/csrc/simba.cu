@@ -1,0 +1,1376 @@
+// simba.cu -- kernels, host runtime and C ABI of libsimba.so (sm_100a).
+//
+// Kernels
+//   unit_kernel<W,E>   the production scan: persistent grid, warps claim
+//                      rank chunks in ascending order, decode one *unit*
+//                      (codec.py:89-133 restructured, see simba_device.cuh)
+//                      warp-uniformly and sweep its ranks across lanes with a
+//                      branch-free LOP3/IMAD spine; __any_sync early exit to
+//                      the per-example check; atomicMin of the first
+//                      satisfying rank / warp-aggregated count.
+//   direct_kernel<W>   one rank per lane, full reference-exact unrank + RPN
+//                      evaluation (the literal per-thread design); used for
+//                      the shuffled (RTid) mode (codec.py:210-236) and as the
+//                      literal-design comparison.
+//   value_table_kernel per-spec super-leaf values (all subtrees of size <= R0
+//                      on the first E examples), built once per context.
+//   decode_kernel      codec.decode of one rank (winner tokens).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "simba_device.cuh"
+
+using namespace simba;
+typedef unsigned __int128 u128;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(SIMBA_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_));     \
+    } while (0)
+
+constexpr uint64_t kShuffleMult = 2246822507ULL;  // codec.py:29
+constexpr int kCtrWords = 8;  // ctr, best, count, visited, units[2], flags, spare
+
+}  // namespace
+
+// ===========================================================================
+// device: shared-memory staging and the per-rank (direct) path
+// ===========================================================================
+
+namespace simba {
+
+struct Staged {
+    const Tabs *t;
+    const void *tbl;
+    const void *xs;  // [n][k] words W
+    const void *ys;  // [n] words W
+};
+
+// blob layout (global): [value tables: tbl_bytes][inputs n*k W][outputs n W]
+struct BlobInfo {
+    const unsigned char *blob;
+    uint32_t tbl_bytes;  // multiple of 16
+    uint32_t ex_bytes;   // multiple of 16
+};
+
+__device__ __forceinline__ void copy16(void *dst, const void *src, uint32_t bytes)
+{
+    const uint4 *s = reinterpret_cast<const uint4 *>(src);
+    uint4 *d = reinterpret_cast<uint4 *>(dst);
+    for (uint32_t i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+        d[i] = s[i];
+}
+
+template <class W>
+__device__ __forceinline__ Staged stage(const KParams &p, const BlobInfo &bi, unsigned char *smem, bool tables)
+{
+    Staged st;
+    Tabs *t = reinterpret_cast<Tabs *>(smem);
+    copy16(t, p.tabs, sizeof(Tabs));
+    unsigned char *cur = smem + sizeof(Tabs);
+    if (tables) {
+        copy16(cur, bi.blob, bi.tbl_bytes);
+        st.tbl = cur;
+        cur += bi.tbl_bytes;
+    } else {
+        st.tbl = bi.blob;
+    }
+    const unsigned char *ex_g = bi.blob + bi.tbl_bytes;
+    if (p.stage_examples) {
+        copy16(cur, ex_g, bi.ex_bytes);
+        st.xs = cur;
+    } else {
+        st.xs = ex_g;
+    }
+    st.ys = reinterpret_cast<const W *>(st.xs) + (size_t)p.n * p.k;
+    st.t = t;
+    __syncthreads();
+    return st;
+}
+
+__device__ __forceinline__ uint64_t shuffle_index(uint64_t i, uint64_t total)
+{
+    return (uint64_t)(((u128)i * kShuffleMult) % total);  // codec.py:232-236
+}
+
+__device__ __forceinline__ void record_hit(const KParams &p, uint64_t rank, uint64_t &my_count)
+{
+    ++my_count;
+    atomicMin(p.best, (unsigned long long)rank);
+}
+
+// One rank per lane over [n0, n1) (local indices when shuffled): reference
+// unrank + evaluation on example 0, then the remaining examples in warp
+// lock-step with __any_sync early exit (expr.py:201-218 short-circuit).
+template <class W>
+__device__ __noinline__ void direct_range(const KParams &p, const Staged &st, uint64_t n0, uint64_t n1,
+                                          bool shuffled, uint64_t &my_count)
+{
+    const int lane = threadIdx.x & 31;
+    const W *xs = reinterpret_cast<const W *>(st.xs);
+    const W *ys = reinterpret_cast<const W *>(st.ys);
+    const W mask = (W)p.mask;
+    int8_t buf[MAXS];
+    for (uint64_t b = n0; b < n1; b += 32) {
+        const uint64_t i = b + lane;
+        const bool act = i < n1;
+        bool alive = false;
+        uint64_t rank = 0;
+        if (act) {
+            rank = shuffled ? p.offset + shuffle_index(i, p.block_total) : i;
+            decode_tokens(st.t, rank, p.s, buf);
+            alive = (((eval_rpn<W, W>(buf, p.s, xs) ^ ys[0]) & mask) == 0);
+        }
+        for (int e = 1; e < p.n; ++e) {
+            if (!__any_sync(FULL, alive))
+                break;
+            if (alive)
+                alive = (((eval_rpn<W, W>(buf, p.s, xs + (size_t)e * p.k) ^ ys[e]) & mask) == 0);
+        }
+        if (alive)
+            record_hit(p, rank, my_count);
+    }
+}
+
+// Reference-exact verification of one rank against every example.
+template <class W>
+__device__ __noinline__ bool full_check(const KParams &p, const Staged &st, uint64_t rank)
+{
+    const W *xs = reinterpret_cast<const W *>(st.xs);
+    const W *ys = reinterpret_cast<const W *>(st.ys);
+    const W mask = (W)p.mask;
+    int8_t buf[MAXS];
+    decode_tokens(st.t, rank, p.s, buf);
+    for (int e = 0; e < p.n; ++e)
+        if (((eval_rpn<W, W>(buf, p.s, xs + (size_t)e * p.k) ^ ys[e]) & mask) != 0)
+            return false;
+    return true;
+}
+
+// ===========================================================================
+// unit sweep
+// ===========================================================================
+
+template <class W, int N>
+__device__ __forceinline__ void bcast_seg_array(const Seg<W> (&in)[N], int src, Seg<W> (&out)[N])
+{
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        out[i].m = __shfl_sync(FULL, in[i].m, src);
+        out[i].x = __shfl_sync(FULL, in[i].x, src);
+        out[i].a = __shfl_sync(FULL, in[i].a, src);
+        out[i].b = __shfl_sync(FULL, in[i].b, src);
+    }
+}
+
+template <class W, int N, int M>
+__device__ __forceinline__ W segs_first(const Seg<W> (&s)[M], W v)
+{
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        v = seg_apply(s[i], v);
+    return v;
+}
+
+// Rare path: at least one lane matched example 0 through the tables.  Refine
+// on examples 1..E-1 (their segments live in lanes 1..E-1 of the odometer),
+// then verify the survivors against every example with the reference-exact
+// evaluator (decode_tokens + eval_rpn).
+template <class W, int E, int POP>
+__device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const Odometer<W, E> &od, uint64_t ubase,
+                                     uint32_t R2, uint32_t off1, uint32_t off2, bool hit, uint32_t d1, uint32_t d2,
+                                     uint64_t &my_count)
+{
+    const W *tbl = reinterpret_cast<const W *>(st.tbl);
+    const W *ys = reinterpret_cast<const W *>(st.ys);
+    const W mask = (W)p.mask;
+#pragma unroll
+    for (int e = 1; e < E; ++e) {
+        Seg<W> so[MAXSO], sl[MAXSL];
+        bcast_seg_array<W, MAXSO>(od.so, e, so);
+        bcast_seg_array<W, MAXSL>(od.sl, e, sl);
+        if (hit) {
+            const W *te = tbl + (size_t)e * p.tbl_len;
+            W vX = (W)0;
+            if constexpr (POP != OP_NONE)
+                vX = segs_apply(sl, te[off1 + d1]);
+            const W v = segs_apply(so, apply_bin_t<W, POP>(vX, te[off2 + d2]));
+            hit = (((v ^ ys[e]) & mask) == 0);
+        }
+    }
+    if (hit) {
+        const uint64_t rank = ubase + (uint64_t)d1 * R2 + d2;
+        if (full_check<W>(p, st, rank))
+            record_hit(p, rank, my_count);
+    }
+}
+
+// Lane-parallel sweep of unit-local indices [u0, u1) (index = d1*R2 + d2) of
+// one unit whose first index decomposes as (d1s, d2s).  NSO / NSL: segments
+// the outer / left chains actually use (the rest are identities, skipped at
+// compile time).  Tables are read through the dynamic shared-memory symbol so
+// the compiler emits LDS.
+template <class W, int E, int POP, int NSO, int NSL>
+__device__ __forceinline__ void sweep_unit(const KParams &p, const Staged &st, const Odometer<W, E> &od,
+                                           const Seg<W> (&so)[MAXSO], const Seg<W> (&sl)[MAXSL], W y0, W mask,
+                                           uint64_t ubase, uint32_t R2, uint32_t off1, uint32_t off2,
+                                           uint32_t d1s, uint32_t d2s, uint32_t u0, uint32_t u1, int lane,
+                                           uint64_t &my_count)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));  // example-0 value table
+    auto value = [&](W vX, W vR) -> W { return segs_first<W, NSO>(so, apply_bin_t<W, POP>(vX, vR)); };
+    auto miss = [&](W v) -> bool { return ((v ^ y0) & mask) != 0; };
+    if (R2 >= 32) {
+        // lanes over d2, d1 warp-uniform (vX hoisted per row)
+        uint32_t dlo = d2s;
+        for (uint32_t d1 = d1s;; ++d1, dlo = 0) {
+            const uint32_t row = d1 * R2;
+            if (row >= u1)
+                break;
+            const uint32_t dhi = min(R2, u1 - row);
+            W vX = (W)0;
+            if constexpr (POP != OP_NONE)
+                vX = segs_first<W, NSL>(sl, t0[off1 + d1]);
+            const W *tr = t0 + off2 + lane;
+            uint32_t it = dlo;
+            for (; it + 128 <= dhi; it += 128) {
+                const W v0 = value(vX, tr[it]);
+                const W v1 = value(vX, tr[it + 32]);
+                const W v2 = value(vX, tr[it + 64]);
+                const W v3 = value(vX, tr[it + 96]);
+                const bool m0 = miss(v0), m1 = miss(v1), m2 = miss(v2), m3 = miss(v3);
+                if (__any_sync(FULL, !(m0 && m1 && m2 && m3))) {
+                    on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, !m0, d1, it + lane, my_count);
+                    on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, !m1, d1, it + 32 + lane, my_count);
+                    on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, !m2, d1, it + 64 + lane, my_count);
+                    on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, !m3, d1, it + 96 + lane, my_count);
+                }
+            }
+            for (; it < dhi; it += 32) {
+                const uint32_t d2 = it + lane;
+                const bool act = d2 < dhi;
+                const bool hit = act && !miss(value(vX, t0[off2 + (act ? d2 : it)]));
+                if (__any_sync(FULL, hit))
+                    on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, hit, d1, d2, my_count);
+            }
+        }
+    } else {
+        // R2 < 32: lanes over (d1, d2) pairs, G rows per step
+        const uint32_t G = 32u / R2;
+        const uint32_t lg = (uint32_t)lane / R2;
+        const uint32_t ld2 = (uint32_t)lane - lg * R2;
+        const bool lane_ok = lg < G;
+        const W vR = t0[off2 + (lane_ok ? ld2 : 0)];
+        for (uint32_t d1b = d1s; d1b * R2 < u1; d1b += 2 * G) {
+            const uint32_t da = d1b + lg, db = d1b + G + lg;
+            const uint32_t ua = da * R2 + ld2, ub = db * R2 + ld2;
+            const bool acta = lane_ok && ua >= u0 && ua < u1;
+            const bool actb = lane_ok && ub >= u0 && ub < u1;
+            W xa = (W)0, xb = (W)0;
+            if constexpr (POP != OP_NONE) {
+                xa = segs_first<W, NSL>(sl, t0[off1 + (acta ? da : d1s)]);
+                xb = segs_first<W, NSL>(sl, t0[off1 + (actb ? db : d1s)]);
+            }
+            const bool ha = acta && !miss(value(xa, vR));
+            const bool hb = actb && !miss(value(xb, vR));
+            if (__any_sync(FULL, ha || hb)) {
+                on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, ha, acta ? da : 0, ld2, my_count);
+                on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, hb, actb ? db : 0, ld2, my_count);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t read_best(const KParams &p)
+{
+    unsigned long long b = 0;
+    if ((threadIdx.x & 31) == 0)
+        b = min(*(volatile unsigned long long *)p.best, (unsigned long long)p.stop_above);
+    return __shfl_sync(FULL, b, 0);
+}
+
+struct SweepStats {
+    uint64_t count, units, rank_units;
+};
+
+// All ranks [n, n1) of one P block (n1 <= pend).  The outer chain and P's
+// operator are fixed for the whole block; the X odometer advances unit by
+// unit inside this function, so consecutive units cost one decode_x step
+// (usually a single level) instead of a dispatch and a decode from the root.
+// Returns the first rank not scanned (n1 unless a search hit allows early exit).
+template <class W, int E, int POP, int NSO>
+__device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, Odometer<W, E> &od, uint64_t n,
+                                            uint64_t n1, int lane, SweepStats &ss)
+{
+    const W y0 = reinterpret_cast<const W *>(st.ys)[0];
+    const W mask = (W)p.mask;
+    Seg<W> so[MAXSO], sl[MAXSL];
+    if constexpr (E == 1) {
+#pragma unroll
+        for (int i = 0; i < MAXSO; ++i)
+            so[i] = od.so[i];
+    } else {
+        bcast_seg_array<W, MAXSO>(od.so, 0, so);
+    }
+    const Tabs *t = st.t;
+    const int prsz = od.prsz;
+    const uint32_t R2 = (uint32_t)t->T[prsz], off2 = t->toff[prsz];
+    const uint64_t pb = od.pb;
+    if constexpr (POP == OP_NONE) {
+        ++ss.units;
+        sweep_unit<W, E, POP, NSO, 0>(p, st, od, so, sl, y0, mask, pb, R2, 0, off2, 0, (uint32_t)(n - pb),
+                                      (uint32_t)(n - pb), (uint32_t)(n1 - pb), lane, ss.count);
+        return n1;
+    } else {
+        const bool early = (p.mode == SIMBA_MODE_SEARCH);
+        while (n < n1) {
+            const uint64_t rel = n - pb;
+            const uint64_t q = div_T(t, prsz, rel);
+            const uint32_t d2s = (uint32_t)(rel - q * R2);
+            if (!od.have_x || q >= od.qend)
+                od.decode_x(q);
+            const uint64_t qb = od.qb;
+            const uint32_t R1 = (uint32_t)t->T[od.sz1], off1 = t->toff[od.sz1];
+            const uint64_t ubase = pb + qb * R2;
+            const uint64_t stop = min(ubase + (uint64_t)R1 * R2, n1);
+            ++ss.units;
+            if (od.ovf_l) {
+                ++ss.rank_units;
+                direct_range<W>(p, st, n, stop, false, ss.count);
+            } else {
+                if constexpr (E == 1) {
+#pragma unroll
+                    for (int i = 0; i < MAXSL; ++i)
+                        sl[i] = od.sl[i];
+                } else {
+                    bcast_seg_array<W, MAXSL>(od.sl, 0, sl);
+                }
+                const uint32_t u0 = (uint32_t)(n - ubase), u1 = (uint32_t)(stop - ubase);
+                const uint32_t d1s = (uint32_t)(q - qb);
+                if (od.nsl == 0)
+                    sweep_unit<W, E, POP, NSO, 0>(p, st, od, so, sl, y0, mask, ubase, R2, off1, off2, d1s, d2s, u0,
+                                                  u1, lane, ss.count);
+                else
+                    sweep_unit<W, E, POP, NSO, MAXSL>(p, st, od, so, sl, y0, mask, ubase, R2, off1, off2, d1s, d2s,
+                                                      u0, u1, lane, ss.count);
+            }
+            n = stop;
+            if (early && n < n1 && n > read_best(p))
+                break;  // everything left ranks above a hit
+        }
+        return n;
+    }
+}
+
+template <class W, int E, int POP>
+__device__ __forceinline__ uint64_t dispatch_nso(const KParams &p, const Staged &st, Odometer<W, E> &od, uint64_t n,
+                                                 uint64_t n1, int lane, SweepStats &ss)
+{
+    if (od.nso == 0)
+        return run_pblock<W, E, POP, 0>(p, st, od, n, n1, lane, ss);
+    if (od.nso == 1)
+        return run_pblock<W, E, POP, 1>(p, st, od, n, n1, lane, ss);
+    if (od.nso == 2)
+        return run_pblock<W, E, POP, 2>(p, st, od, n, n1, lane, ss);
+    return run_pblock<W, E, POP, 4>(p, st, od, n, n1, lane, ss);
+}
+
+template <class W, int E>
+__device__ __noinline__ uint64_t process_pblock(const KParams &p, const Staged &st, Odometer<W, E> &od, uint64_t n,
+                                                uint64_t n1, int lane, SweepStats &ss)
+{
+    switch (od.pop) {
+    case OP_AND: return dispatch_nso<W, E, OP_AND>(p, st, od, n, n1, lane, ss);
+    case OP_OR: return dispatch_nso<W, E, OP_OR>(p, st, od, n, n1, lane, ss);
+    case OP_XOR: return dispatch_nso<W, E, OP_XOR>(p, st, od, n, n1, lane, ss);
+    case OP_ADD: return dispatch_nso<W, E, OP_ADD>(p, st, od, n, n1, lane, ss);
+    case OP_SUB: return dispatch_nso<W, E, OP_SUB>(p, st, od, n, n1, lane, ss);
+    case OP_MUL: return dispatch_nso<W, E, OP_MUL>(p, st, od, n, n1, lane, ss);
+    default: return dispatch_nso<W, E, OP_NONE>(p, st, od, n, n1, lane, ss);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// work distribution: guided claims of virtual chunks
+// ---------------------------------------------------------------------------
+//
+// The range [lo, hi) is cut into chunks of chunk_len ranks, grouped into
+// super-chunks of `spc` chunks; this shard owns super-chunks
+// sc = shard, shard + nshards, ... (round robin) and numbers its chunks
+// 0..nvirt-1 in ascending rank order.  Warps claim runs of virtual chunks from
+// one counter; the run length shrinks with the remaining work (guided
+// self-scheduling), so early claims are long contiguous scans (the odometer
+// state survives across them) and the tail is fine-grained.
+
+struct Claim {
+    uint64_t v0, v1;  // virtual chunk run [v0, v1)
+};
+
+constexpr uint64_t kGuide = 16;  // claim ~ remaining / (warps * kGuide)
+
+__device__ __forceinline__ bool claim_run(const KParams &p, uint64_t t0, uint64_t &hint, Claim &cl)
+{
+    const int lane = threadIdx.x & 31;
+    unsigned long long c = 0;
+    int go = 1;
+    if (lane == 0) {
+        const uint64_t want = hint;
+        c = atomicAdd(p.ctr, (unsigned long long)want);
+        if (c >= p.nvirt) {
+            go = 0;
+        } else {
+            cl.v0 = c;
+            cl.v1 = min((uint64_t)(c + want), p.nvirt);
+            const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+            hint = (p.nvirt - cl.v1) / (warps * kGuide);
+            if (hint < 1)
+                hint = 1;
+            // the time budget is polled between runs only and never masks a
+            // recorded hit; the very first run always proceeds (engine.py:251-258)
+            if (p.budget_ns && c > 0 && *(volatile unsigned long long *)p.best == SIMBA_NO_RANK &&
+                globaltimer_ns() - t0 > p.budget_ns) {
+                atomicOr(p.flags, 1u);
+                go = 0;
+            }
+        }
+    }
+    go = __shfl_sync(FULL, go, 0);
+    cl.v0 = __shfl_sync(FULL, cl.v0, 0);
+    cl.v1 = __shfl_sync(FULL, cl.v1, 0);
+    hint = __shfl_sync(FULL, hint, 0);
+    return go != 0;
+}
+
+// real rank range of the contiguous piece of a run starting at virtual chunk v
+__device__ __forceinline__ void run_piece(const KParams &p, uint64_t v, uint64_t v1, uint64_t &c0, uint64_t &c1,
+                                          uint64_t &vnext)
+{
+    const uint64_t sc = v / p.spc, within = v - sc * p.spc;
+    const uint64_t pend = min(v1, (sc + 1) * p.spc);
+    const uint64_t rc = (p.shard + sc * p.nshards) * p.spc + within;
+    c0 = p.lo + rc * p.chunk_len;
+    c1 = min(p.lo + (rc + (pend - v)) * p.chunk_len, p.hi);
+    if (c0 > p.hi)
+        c0 = p.hi;
+    vnext = pend;
+}
+
+__device__ __forceinline__ void flush_counts(const KParams &p, uint64_t my_count, uint64_t vis, uint64_t units,
+                                             uint64_t direct_units)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+        my_count += __shfl_xor_sync(FULL, my_count, o);
+    if ((threadIdx.x & 31) == 0) {
+        if (my_count)
+            atomicAdd(p.count, (unsigned long long)my_count);
+        if (vis)
+            atomicAdd(p.visited, (unsigned long long)vis);
+        if (units)
+            atomicAdd(&p.units[0], (unsigned long long)units);
+        if (direct_units)
+            atomicAdd(&p.units[1], (unsigned long long)direct_units);
+    }
+}
+
+template <class W, int E>
+__global__ void __launch_bounds__(256, 2) unit_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Staged st = stage<W>(p, bi, smem, true);
+    const int lane = threadIdx.x & 31;
+    Odometer<W, E> od;
+    od.L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
+    od.t = st.t;
+    od.tbl_e = reinterpret_cast<const W *>(st.tbl) + (size_t)(lane & (E - 1)) * p.tbl_len;
+    od.R0 = p.R0;
+    od.s = p.s;
+    od.lane = lane;
+    od.ex = lane & (E - 1);
+    const bool early = (p.mode == SIMBA_MODE_SEARCH);
+    const uint64_t t0 = globaltimer_ns();
+    SweepStats ss{0, 0, 0};
+    uint64_t vis = 0;
+    uint64_t hint = p.nvirt / ((uint64_t)gridDim.x * (blockDim.x >> 5) * kGuide);
+    if (hint < 1)
+        hint = 1;
+    Claim cl;
+    bool stop = false;
+    while (!stop && claim_run(p, t0, hint, cl)) {
+        for (uint64_t v = cl.v0; v < cl.v1 && !stop;) {
+            uint64_t c0, c1, vn;
+            run_piece(p, v, cl.v1, c0, c1, vn);
+            v = vn;
+            if (c0 >= c1)
+                continue;
+            if (early && c0 > read_best(p)) {
+                stop = true;
+                break;
+            }
+            od.reset();
+            uint64_t n = c0;
+            while (n < c1) {
+                od.outer_at(n);
+                const uint64_t pstop = min(od.pend, c1);
+                if (od.ovf_o) {
+                    ++ss.units;
+                    ++ss.rank_units;
+                    direct_range<W>(p, st, n, pstop, false, ss.count);
+                    n = pstop;
+                } else {
+                    n = process_pblock<W, E>(p, st, od, n, pstop, lane, ss);
+                }
+                if (early && n < c1 && n > read_best(p))
+                    break;  // everything left in this piece ranks above a hit
+            }
+            vis += n - c0;
+        }
+    }
+    flush_counts(p, ss.count, vis, ss.units, ss.rank_units);
+}
+
+template <class W>
+__global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Staged st = stage<W>(p, bi, smem, false);
+    const bool early = (p.mode == SIMBA_MODE_SEARCH) && !p.shuffled;
+    const uint64_t t0 = globaltimer_ns();
+    uint64_t my_count = 0, vis = 0;
+    uint64_t hint = p.nvirt / ((uint64_t)gridDim.x * (blockDim.x >> 5) * kGuide);
+    if (hint < 1)
+        hint = 1;
+    Claim cl;
+    bool stop = false;
+    while (!stop && claim_run(p, t0, hint, cl)) {
+        for (uint64_t v = cl.v0; v < cl.v1;) {
+            uint64_t c0, c1, vn;
+            run_piece(p, v, cl.v1, c0, c1, vn);
+            v = vn;
+            if (c0 >= c1)
+                continue;
+            if (early && c0 > read_best(p)) {
+                stop = true;
+                break;
+            }
+            direct_range<W>(p, st, c0, c1, p.shuffled != 0, my_count);
+            vis += c1 - c0;
+        }
+    }
+    flush_counts(p, my_count, vis, 0, 0);
+}
+
+
+template <class W>
+__global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int R0, int E, uint32_t tbl_len, W *out)
+{
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (uint32_t)E * tbl_len)
+        return;
+    const uint32_t e = idx / tbl_len;
+    const uint32_t j = idx - e * tbl_len;
+    int sz = 1;
+    while (sz < R0 && tabs->toff[sz + 1] <= j)
+        ++sz;
+    int8_t buf[MAXS];
+    decode_tokens(tabs, j - tabs->toff[sz], sz, buf);
+    out[idx] = eval_rpn<W, W>(buf, sz, X + (size_t)e * k);
+}
+
+__global__ void decode_kernel(const Tabs *tabs, uint64_t rank, int size, int32_t *out)
+{
+    int8_t buf[MAXS];
+    decode_tokens(tabs, rank, size, buf);
+    for (int i = 0; i < size; ++i)
+        out[i] = buf[i];
+}
+
+}  // namespace simba
+
+// ===========================================================================
+// host
+// ===========================================================================
+
+namespace {
+
+struct Magic {
+    uint64_t m64;
+    uint32_t m32;
+    uint8_t sh1, sh2;
+};
+
+// Granlund & Montgomery (PLDI'94, Fig. 4.1) round-down division by d >= 1.
+Magic gm_magic(uint64_t d)
+{
+    Magic g{};
+    int l = 0;
+    while (l < 64 && ((u128)1 << l) < d)
+        ++l;
+    g.m64 = (uint64_t)(((((u128)1 << l) - d) << 64) / d + 1);
+    if (d < ((uint64_t)1 << 32))
+        g.m32 = (uint32_t)((((((uint64_t)1) << l) - d) << 32) / d + 1);
+    g.sh1 = (uint8_t)std::min(l, 1);
+    g.sh2 = (uint8_t)std::max(l - 1, 0);
+    return g;
+}
+
+// counting.py:88-128 with the reference's 128-bit cap; rows[s][0..8].
+int build_rows(int k, int max_size, std::vector<std::array<u128, 9>> &rows, int *err_s, int *err_op)
+{
+    rows.assign(max_size + 1, {});
+    rows[1][8] = (u128)k;
+    for (int s = 2; s <= max_size; ++s) {
+        bool ovc = false, ovs = false, ovt = false;
+        u128 unary = rows[s - 1][8], comm = 0, sub = 0, p;
+        for (int j = 1; j <= (s - 1) / 2; ++j)
+            if (__builtin_mul_overflow(rows[j][8], rows[s - 1 - j][8], &p) || __builtin_add_overflow(comm, p, &comm))
+                ovc = true;
+        for (int j = 1; j <= s - 2; ++j)
+            if (__builtin_mul_overflow(rows[j][8], rows[s - 1 - j][8], &p) || __builtin_add_overflow(sub, p, &sub))
+                ovs = true;
+        u128 total = 0, a;
+        if (__builtin_mul_overflow(unary, (u128)2, &a) || __builtin_add_overflow(total, a, &total))
+            ovt = true;
+        if (__builtin_mul_overflow(comm, (u128)5, &a) || __builtin_add_overflow(total, a, &total))
+            ovt = true;
+        if (__builtin_add_overflow(total, sub, &total))
+            ovt = true;
+        if (ovc || ovs || ovt) {
+            if (err_s)
+                *err_s = s;
+            if (err_op)
+                *err_op = ovc ? 1 : ovs ? 6 : 8;  // first slot in 0..8 order
+            return SIMBA_ECAPACITY;
+        }
+        rows[s][0] = rows[s][4] = unary;
+        rows[s][1] = rows[s][2] = rows[s][3] = rows[s][5] = rows[s][7] = comm;
+        rows[s][6] = sub;
+        rows[s][8] = total;
+    }
+    return SIMBA_OK;
+}
+
+}  // namespace
+
+struct simba_ctx {
+    int device = 0, k = 0, w = 0, n = 0, max_size = 0;
+    int wbytes = 4, R0 = 1, E = 1, kernel = 0;
+    uint32_t tbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
+    int block_threads = 256, grid_unit = 0, grid_direct = 0;
+    int smem_unit = 0, smem_direct = 0;
+    uint32_t lvl_off = 0;
+    bool stage_examples = true;
+    uint64_t mask = 0;
+    std::vector<std::array<u128, 9>> rows;
+    Tabs h_tabs{};
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    Tabs *d_tabs = nullptr;
+    unsigned char *d_blob = nullptr;
+    unsigned long long *d_ctr = nullptr;
+    unsigned long long *h_ctr = nullptr;
+    int32_t *d_tok = nullptr;
+};
+
+namespace {
+
+template <class W>
+int setup_kernels(simba_ctx *c)
+{
+    CK(cudaFuncSetAttribute(unit_kernel<W, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_unit));
+    CK(cudaFuncSetAttribute(unit_kernel<W, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_unit));
+    CK(cudaFuncSetAttribute(unit_kernel<W, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_unit));
+    CK(cudaFuncSetAttribute(direct_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_direct));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    int bu = 0, bd = 0;
+    const void *uk = (c->E == 1) ? (const void *)unit_kernel<W, 1>
+                     : (c->E == 2) ? (const void *)unit_kernel<W, 2>
+                                   : (const void *)unit_kernel<W, 4>;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, uk, c->block_threads, c->smem_unit));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bd, (const void *)direct_kernel<W>, c->block_threads,
+                                                     c->smem_direct));
+    if (bu < 1 || bd < 1)
+        return fail(SIMBA_ECUDA, "kernel does not fit on an SM (smem %d bytes)", c->smem_unit);
+    c->grid_unit = sms * bu;
+    c->grid_direct = sms * bd;
+    return SIMBA_OK;
+}
+
+template <class W>
+int build_value_tables(simba_ctx *c)
+{
+    const uint32_t total = (uint32_t)c->E * c->tbl_len;
+    const int bt = 128;
+    value_table_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(
+        c->d_tabs, reinterpret_cast<const W *>(c->d_blob + c->tbl_bytes), c->k, c->R0, c->E, c->tbl_len,
+        reinterpret_cast<W *>(c->d_blob));
+    g_launches++;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    return SIMBA_OK;
+}
+
+template <class W>
+void launch_scan(simba_ctx *c, const KParams &p, const BlobInfo &bi, bool direct)
+{
+    if (direct) {
+        direct_kernel<W><<<c->grid_direct, c->block_threads, c->smem_direct, c->stream>>>(p, bi);
+    } else if (c->E == 1) {
+        unit_kernel<W, 1><<<c->grid_unit, c->block_threads, c->smem_unit, c->stream>>>(p, bi);
+    } else if (c->E == 2) {
+        unit_kernel<W, 2><<<c->grid_unit, c->block_threads, c->smem_unit, c->stream>>>(p, bi);
+    } else {
+        unit_kernel<W, 4><<<c->grid_unit, c->block_threads, c->smem_unit, c->stream>>>(p, bi);
+    }
+    g_launches++;
+}
+
+uint64_t row_total(const simba_ctx *c, int s) { return (uint64_t)c->rows[s][8]; }
+
+struct Req {
+    int size;
+    int mode;
+    uint64_t lo, hi;  // local indices when shuffled, in-size ranks otherwise
+    uint64_t chunk, shard, nshards, stop_above;
+    double budget_s;
+    bool shuffled;
+    uint64_t offset, block_total;
+    bool direct;
+};
+
+int decode_rank(simba_ctx *c, uint64_t rank, int size, int32_t *tokens)
+{
+    decode_kernel<<<1, 1, 0, c->stream>>>(c->d_tabs, rank, size, c->d_tok);
+    g_launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(tokens, c->d_tok, sizeof(int32_t) * size, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SIMBA_OK;
+}
+
+int run_req(simba_ctx *c, const Req &rq, simba_result *out)
+{
+    memset(out, 0, sizeof(*out));
+    out->best_rank = SIMBA_NO_RANK;
+    out->size = rq.size;
+    out->completed = 1;
+    if (rq.size < 1 || rq.size > c->max_size)
+        return fail(SIMBA_ERANGE, "size %d outside 1..%d", rq.size, c->max_size);
+    const uint64_t tot = row_total(c, rq.size);
+    if (rq.shuffled) {
+        if (rq.block_total == 0 || rq.offset > tot || rq.block_total > tot - rq.offset || rq.hi > rq.block_total)
+            return fail(SIMBA_ERANGE, "block [%llu,+%llu) outside size %d", (unsigned long long)rq.offset,
+                        (unsigned long long)rq.block_total, rq.size);
+    } else if (rq.hi > tot) {
+        return fail(SIMBA_ERANGE, "rank %llu beyond T[%d][8]=%llu", (unsigned long long)rq.hi, rq.size,
+                    (unsigned long long)tot);
+    }
+    if (rq.lo > rq.hi)
+        return fail(SIMBA_EINVAL, "empty-range bounds reversed");
+    if (rq.nshards < 1 || rq.shard >= rq.nshards)
+        return fail(SIMBA_EINVAL, "bad shard %llu of %llu", (unsigned long long)rq.shard,
+                    (unsigned long long)rq.nshards);
+    if (rq.lo == rq.hi)
+        return SIMBA_OK;
+    CK(cudaSetDevice(c->device));
+    const bool direct = rq.direct || rq.shuffled || c->kernel == 1;
+    const uint64_t range = rq.hi - rq.lo;
+    const uint64_t warps = (uint64_t)(direct ? c->grid_direct : c->grid_unit) * (c->block_threads / 32);
+    // chunk = claim granularity; super-chunk = sharding unit (round robin)
+    uint64_t chunk, spc;
+    if (rq.chunk) {
+        chunk = rq.chunk;
+        spc = (rq.nshards > 1) ? 1 : (range + chunk - 1) / chunk;
+    } else {
+        const uint64_t target = range / (warps * 64 * rq.nshards) + 1;
+        chunk = 256;
+        while (chunk < target && chunk < (1ull << 20))
+            chunk <<= 1;
+        spc = 1;
+        if (rq.nshards > 1) {
+            const uint64_t per = range / (rq.nshards * 16) + 1;  // ~16 super-chunks per shard
+            while (spc * chunk < per && spc < (1ull << 20))
+                spc <<= 1;
+        } else {
+            spc = (range + chunk - 1) / chunk;
+        }
+    }
+    const uint64_t nchunks = (range + chunk - 1) / chunk;
+    const uint64_t nsuper = (nchunks + spc - 1) / spc;
+    const uint64_t owned = (rq.shard < nsuper) ? (nsuper - rq.shard + rq.nshards - 1) / rq.nshards : 0;
+    KParams p{};
+    p.tabs = c->d_tabs;
+    p.tbl = c->d_blob;
+    p.tbl_len = c->tbl_len;
+    p.k = c->k;
+    p.n = c->n;
+    p.s = rq.size;
+    p.R0 = std::min(c->R0, rq.size);
+    p.E = c->E;
+    p.mode = rq.mode;
+    p.shuffled = rq.shuffled ? 1 : 0;
+    p.mask = c->mask;
+    p.lo = rq.lo;
+    p.hi = rq.hi;
+    p.chunk_len = chunk;
+    p.spc = spc;
+    p.nvirt = owned * spc;
+    p.lvl_off = c->lvl_off;
+    p.shard = rq.shard;
+    p.nshards = rq.nshards;
+    p.stop_above = rq.stop_above;
+    p.offset = rq.offset;
+    p.block_total = rq.block_total;
+    p.budget_ns = 0;
+    if (rq.budget_s >= 0)
+        p.budget_ns = std::max<uint64_t>(1, (uint64_t)(rq.budget_s * 1e9));
+    p.stage_examples = c->stage_examples ? 1 : 0;
+    p.ctr = c->d_ctr + 0;
+    p.best = c->d_ctr + 1;
+    p.count = c->d_ctr + 2;
+    p.visited = c->d_ctr + 3;
+    p.units = c->d_ctr + 4;
+    p.flags = reinterpret_cast<unsigned int *>(c->d_ctr + 6);
+    BlobInfo bi{c->d_blob, c->tbl_bytes, c->ex_bytes};
+    const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(c->d_ctr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaEventRecord(c->ev0, c->stream));
+    if (c->wbytes == 4)
+        launch_scan<uint32_t>(c, p, bi, direct);
+    else
+        launch_scan<uint64_t>(c, p, bi, direct);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev1, c->stream));
+    CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(unsigned long long) * kCtrWords, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    out->kernel_ms = ms;
+    out->launches = 1;
+    out->visited = c->h_ctr[3];
+    out->units = c->h_ctr[4];
+    out->rank_units = c->h_ctr[5];
+    out->count = c->h_ctr[2];
+    out->best_rank = c->h_ctr[1];
+    out->completed = (c->h_ctr[6] & 1u) ? 0 : 1;
+    out->found = out->best_rank != SIMBA_NO_RANK;
+    if (out->found) {
+        int rc = decode_rank(c, out->best_rank, rq.size, out->tokens);
+        if (rc)
+            return rc;
+        out->launches += 1;
+    }
+    return SIMBA_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+
+extern "C" {
+
+const char *simba_last_error(void) { return g_err.c_str(); }
+
+uint64_t simba_launch_count(void) { return g_launches.load(); }
+
+int simba_device_count(void)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int simba_table_build(int k, int max_size, uint64_t *rows_lo, uint64_t *rows_hi, uint64_t *cum_lo,
+                      uint64_t *cum_hi, int *err_s, int *err_op)
+{
+    if (k < 1)
+        return fail(SIMBA_EINVAL, "variable count must be >= 1, got %d", k);
+    if (max_size < 1)
+        return fail(SIMBA_EINVAL, "max_size must be >= 1, got %d", max_size);
+    if (max_size > SIMBA_TABLE_MAX)
+        return fail(SIMBA_EINVAL, "max_size %d beyond the supported extent %d", max_size, SIMBA_TABLE_MAX);
+    std::vector<std::array<u128, 9>> rows;
+    int rc = build_rows(k, max_size, rows, err_s, err_op);
+    if (rc)
+        return fail(rc, "count T[%d][%d] exceeds 128-bit capacity", err_s ? *err_s : -1, err_op ? *err_op : -1);
+    u128 acc = 0;
+    for (int s = 0; s <= max_size; ++s) {
+        for (int op = 0; op < 9; ++op) {
+            rows_lo[s * 9 + op] = (uint64_t)rows[s][op];
+            rows_hi[s * 9 + op] = (uint64_t)(rows[s][op] >> 64);
+        }
+        if (s >= 1)
+            acc += rows[s][8];
+        cum_lo[s] = (uint64_t)acc;
+        cum_hi[s] = (uint64_t)(acc >> 64);
+    }
+    return SIMBA_OK;
+}
+
+int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t *outputs, int max_size,
+                     const simba_options *opt, simba_ctx **out)
+{
+    *out = nullptr;
+    // Specification.__post_init__ (engine.py:52-67)
+    if (k < 1)
+        return fail(SIMBA_EINVAL, "variable count must be >= 1, got %d", k);
+    if (w < 1 || w > 64)
+        return fail(SIMBA_EINVAL, "bit width must be in 1..64, got %d", w);
+    if (n < 1)
+        return fail(SIMBA_EINVAL, "specification needs at least one pair");
+    if (k > 64)
+        return fail(SIMBA_EINVAL, "device path supports k <= 64 variables, got %d", k);
+    if (max_size < 1 || max_size > SIMBA_MAX_SIZE)
+        return fail(SIMBA_ERANGE, "max_size %d outside device extent 1..%d", max_size, SIMBA_MAX_SIZE);
+    const uint64_t mask = (w == 64) ? ~0ULL : ((1ULL << w) - 1);
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < k; ++j)
+            if (inputs[(size_t)i * k + j] & ~mask)
+                return fail(SIMBA_EINVAL, "value %llu does not fit in %d bits",
+                            (unsigned long long)inputs[(size_t)i * k + j], w);
+        if (outputs[i] & ~mask)
+            return fail(SIMBA_EINVAL, "value %llu does not fit in %d bits", (unsigned long long)outputs[i], w);
+    }
+    {
+        std::vector<int> idx(n);
+        for (int i = 0; i < n; ++i)
+            idx[i] = i;
+        auto key_less = [&](int a, int b) {
+            return std::lexicographical_compare(inputs + (size_t)a * k, inputs + (size_t)a * k + k,
+                                                inputs + (size_t)b * k, inputs + (size_t)b * k + k);
+        };
+        std::sort(idx.begin(), idx.end(), key_less);
+        for (int i = 1; i < n; ++i)
+            if (std::equal(inputs + (size_t)idx[i] * k, inputs + (size_t)idx[i] * k + k,
+                           inputs + (size_t)idx[i - 1] * k))
+                return fail(SIMBA_EINVAL, "duplicate input tuple (pair %d)", idx[i]);
+    }
+    simba_options o{};
+    if (opt)
+        o = *opt;
+    simba_ctx *c = new simba_ctx();
+    auto bail = [&](int rc) {
+        simba_ctx_destroy(c);
+        return rc;
+    };
+    c->device = o.device;
+    c->k = k;
+    c->w = w;
+    c->n = n;
+    c->max_size = max_size;
+    c->mask = mask;
+    c->wbytes = (w <= 32) ? 4 : 8;
+    c->kernel = o.kernel;
+    int es = 0, eo = 0;
+    if (build_rows(k, max_size, c->rows, &es, &eo))
+        return bail(fail(SIMBA_ECAPACITY, "count T[%d][%d] exceeds 128-bit capacity", es, eo));
+    for (int s = 1; s <= max_size; ++s)
+        if (c->rows[s][8] >> 64)
+            return bail(fail(SIMBA_ERANGE, "T[%d][8] >= 2^64: beyond the 64-bit rank space of the device path", s));
+    // decoder tables
+    Tabs &t = c->h_tabs;
+    memset(&t, 0, sizeof(t));
+    for (int s = 1; s <= max_size; ++s) {
+        t.T[s] = (uint64_t)c->rows[s][8];
+        Magic g = gm_magic(t.T[s]);
+        t.m64[s] = g.m64;
+        t.m32[s] = g.m32;
+        t.sh1[s] = g.sh1;
+        t.sh2[s] = g.sh2;
+        uint64_t run = 0;
+        for (int op = 0; op < 8; ++op) {
+            run += (uint64_t)c->rows[s][op];
+            t.slot_cum[s][op] = run;
+        }
+        run = 0;
+        for (int j = 1; j <= s - 2; ++j) {
+            run += (uint64_t)(c->rows[j][8] * c->rows[s - 1 - j][8]);
+            t.split_cum[s][j] = run;
+        }
+    }
+    // examples with value tables
+    int E = o.table_examples;
+    if (E == 0) {
+        bool low = (w <= 16);
+        for (int j = 0; j < k; ++j)
+            if (inputs[j] < 4096)
+                low = true;
+        if (outputs[0] < 4096)
+            low = true;
+        E = low ? 4 : 1;
+    }
+    if (E != 1 && E != 2 && E != 4)
+        return bail(fail(SIMBA_EINVAL, "table_examples must be 1, 2 or 4, got %d", E));
+    while (E > n)
+        E >>= 1;
+    c->E = E;
+    // super-leaf cut-off: largest R0 whose E value tables fit the budget and
+    // whose per-size counts keep unit-local indices in 32 bits
+    const uint64_t budget = 64 * 1024;
+    int R0 = o.r0;
+    auto tbl_size = [&](int r) {
+        uint64_t s = 0;
+        for (int z = 1; z <= r; ++z)
+            s += t.T[z];
+        return s;
+    };
+    if (R0 == 0) {
+        R0 = 1;
+        for (int r = 2; r <= max_size; ++r) {
+            if (t.T[r] > 65535 || tbl_size(r) * E * c->wbytes > budget)
+                break;
+            R0 = r;
+        }
+    } else {
+        if (R0 < 1 || R0 > max_size)
+            return bail(fail(SIMBA_EINVAL, "r0 %d outside 1..%d", R0, max_size));
+        for (int r = 1; r <= R0; ++r)
+            if (t.T[r] > 65535)
+                return bail(fail(SIMBA_EINVAL, "r0 %d: T[%d] exceeds 65535", R0, r));
+        if (tbl_size(R0) * E * c->wbytes > 200 * 1024)
+            return bail(fail(SIMBA_EINVAL, "r0 %d: value tables exceed shared memory", R0));
+    }
+    c->R0 = R0;
+    {
+        uint32_t off = 0;
+        for (int z = 1; z <= MAXS; ++z) {
+            t.toff[z] = off;
+            if (z <= R0)
+                off += (uint32_t)t.T[z];
+        }
+        c->tbl_len = off;
+    }
+    auto pad16 = [](uint64_t b) { return (uint32_t)((b + 15) & ~15ull); };
+    c->tbl_bytes = pad16((uint64_t)E * c->tbl_len * c->wbytes);
+    c->ex_bytes = pad16((uint64_t)n * (k + 1) * c->wbytes);
+    c->stage_examples = c->ex_bytes <= 32 * 1024;
+    c->block_threads = o.block_threads ? o.block_threads : 256;
+    if (c->block_threads % 32 || c->block_threads < 32 || c->block_threads > 256)
+        return bail(fail(SIMBA_EINVAL, "block_threads must be a multiple of 32 in 32..256"));
+    c->lvl_off = (uint32_t)(sizeof(Tabs) + c->tbl_bytes + (c->stage_examples ? c->ex_bytes : 0));
+    {
+        size_t lv = 0;
+        if (c->wbytes == 4)
+            lv = (E == 1) ? sizeof(WarpLevels<uint32_t, 1>) : (E == 2) ? sizeof(WarpLevels<uint32_t, 2>)
+                                                                     : sizeof(WarpLevels<uint32_t, 4>);
+        else
+            lv = (E == 1) ? sizeof(WarpLevels<uint64_t, 1>) : (E == 2) ? sizeof(WarpLevels<uint64_t, 2>)
+                                                                     : sizeof(WarpLevels<uint64_t, 4>);
+        c->smem_unit = (int)(c->lvl_off + lv * (c->block_threads / 32));
+    }
+    c->smem_direct = (int)(sizeof(Tabs) + (c->stage_examples ? c->ex_bytes : 0));
+    // device state
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return bail(fail(SIMBA_ECUDA, "no CUDA device available (the SIMBA path has no CPU fallback)"));
+    }
+    if (c->device < 0 || c->device >= ndev)
+        return bail(fail(SIMBA_EINVAL, "device %d outside 0..%d", c->device, ndev - 1));
+    auto cuda_bail = [&](cudaError_t e, const char *what) {
+        return bail(fail(SIMBA_ECUDA, "%s: %s", what, cudaGetErrorString(e)));
+    };
+    cudaError_t e;
+    if ((e = cudaSetDevice(c->device)) != cudaSuccess)
+        return cuda_bail(e, "cudaSetDevice");
+    if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_bail(e, "cudaStreamCreate");
+    if ((e = cudaEventCreate(&c->ev0)) != cudaSuccess || (e = cudaEventCreate(&c->ev1)) != cudaSuccess)
+        return cuda_bail(e, "cudaEventCreate");
+    if ((e = cudaMalloc(&c->d_tabs, sizeof(Tabs))) != cudaSuccess)
+        return cuda_bail(e, "cudaMalloc(tabs)");
+    if ((e = cudaMalloc(&c->d_blob, (size_t)c->tbl_bytes + c->ex_bytes)) != cudaSuccess)
+        return cuda_bail(e, "cudaMalloc(blob)");
+    if ((e = cudaMalloc(&c->d_ctr, sizeof(unsigned long long) * kCtrWords)) != cudaSuccess)
+        return cuda_bail(e, "cudaMalloc(counters)");
+    if ((e = cudaMalloc(&c->d_tok, sizeof(int32_t) * MAXS)) != cudaSuccess)
+        return cuda_bail(e, "cudaMalloc(tokens)");
+    if ((e = cudaMallocHost(&c->h_ctr, sizeof(unsigned long long) * kCtrWords)) != cudaSuccess)
+        return cuda_bail(e, "cudaMallocHost");
+    // examples as words W: inputs [n][k] then outputs [n]
+    std::vector<unsigned char> ex(c->ex_bytes, 0);
+    for (int i = 0; i < n * k; ++i) {
+        if (c->wbytes == 4) {
+            uint32_t v = (uint32_t)inputs[i];
+            memcpy(&ex[(size_t)i * 4], &v, 4);
+        } else {
+            memcpy(&ex[(size_t)i * 8], &inputs[i], 8);
+        }
+    }
+    for (int i = 0; i < n; ++i) {
+        const size_t at = ((size_t)n * k + i) * c->wbytes;
+        if (c->wbytes == 4) {
+            uint32_t v = (uint32_t)outputs[i];
+            memcpy(&ex[at], &v, 4);
+        } else {
+            memcpy(&ex[at], &outputs[i], 8);
+        }
+    }
+    if ((e = cudaMemcpyAsync(c->d_tabs, &t, sizeof(Tabs), cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
+        return cuda_bail(e, "upload tables");
+    if ((e = cudaMemcpyAsync(c->d_blob + c->tbl_bytes, ex.data(), c->ex_bytes, cudaMemcpyHostToDevice,
+                             c->stream)) != cudaSuccess)
+        return cuda_bail(e, "upload examples");
+    int rc = (c->wbytes == 4) ? build_value_tables<uint32_t>(c) : build_value_tables<uint64_t>(c);
+    if (rc)
+        return bail(rc);
+    rc = (c->wbytes == 4) ? setup_kernels<uint32_t>(c) : setup_kernels<uint64_t>(c);
+    if (rc)
+        return bail(rc);
+    if (o.blocks_per_sm > 0) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+        c->grid_unit = std::min(c->grid_unit, sms * o.blocks_per_sm);
+        c->grid_direct = std::min(c->grid_direct, sms * o.blocks_per_sm);
+    }
+    *out = c;
+    return SIMBA_OK;
+}
+
+void simba_ctx_destroy(simba_ctx *c)
+{
+    if (!c)
+        return;
+    if (c->stream)
+        cudaSetDevice(c->device);
+    if (c->d_tabs)
+        cudaFree(c->d_tabs);
+    if (c->d_blob)
+        cudaFree(c->d_blob);
+    if (c->d_ctr)
+        cudaFree(c->d_ctr);
+    if (c->d_tok)
+        cudaFree(c->d_tok);
+    if (c->h_ctr)
+        cudaFreeHost(c->h_ctr);
+    if (c->ev0)
+        cudaEventDestroy(c->ev0);
+    if (c->ev1)
+        cudaEventDestroy(c->ev1);
+    if (c->stream)
+        cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int simba_ctx_info(simba_ctx *c, int *r0, int *table_examples, int *word_bytes, int *grid_blocks,
+                   int *block_threads, int *smem_bytes)
+{
+    if (!c)
+        return fail(SIMBA_EINVAL, "null context");
+    if (r0)
+        *r0 = c->R0;
+    if (table_examples)
+        *table_examples = c->E;
+    if (word_bytes)
+        *word_bytes = c->wbytes;
+    if (grid_blocks)
+        *grid_blocks = c->kernel == 1 ? c->grid_direct : c->grid_unit;
+    if (block_threads)
+        *block_threads = c->block_threads;
+    if (smem_bytes)
+        *smem_bytes = c->kernel == 1 ? c->smem_direct : c->smem_unit;
+    return SIMBA_OK;
+}
+
+int simba_scan_range(simba_ctx *c, int size, uint64_t offset, uint64_t block_total, uint64_t start, uint64_t stop,
+                     int shuffled, simba_result *out)
+{
+    if (!c)
+        return fail(SIMBA_EINVAL, "null context");
+    if (start > stop || stop > block_total)
+        return fail(SIMBA_ERANGE, "chunk [%llu,%llu) outside block of %llu", (unsigned long long)start,
+                    (unsigned long long)stop, (unsigned long long)block_total);
+    Req rq{};
+    rq.size = size;
+    rq.mode = SIMBA_MODE_SEARCH;
+    rq.nshards = 1;
+    rq.stop_above = SIMBA_NO_RANK;
+    rq.budget_s = -1;
+    if (shuffled) {
+        rq.shuffled = true;
+        rq.lo = start;
+        rq.hi = stop;
+        rq.offset = offset;
+        rq.block_total = block_total;
+    } else {
+        if (offset > UINT64_MAX - stop)
+            return fail(SIMBA_ERANGE, "rank overflow");
+        rq.lo = offset + start;
+        rq.hi = offset + stop;
+    }
+    int rc = run_req(c, rq, out);
+    if (rc == SIMBA_OK)
+        out->visited = stop - start;  // _scan_range reports the whole chunk as visited
+    return rc;
+}
+
+int simba_run(simba_ctx *c, const simba_range *req, simba_result *out)
+{
+    if (!c || !req)
+        return fail(SIMBA_EINVAL, "null argument");
+    if (req->mode != SIMBA_MODE_SEARCH && req->mode != SIMBA_MODE_COUNT)
+        return fail(SIMBA_EINVAL, "unknown mode %d", req->mode);
+    Req rq{};
+    rq.size = req->size;
+    rq.mode = req->mode;
+    rq.lo = req->lo;
+    rq.hi = req->hi;
+    rq.chunk = req->chunk;
+    rq.shard = req->shard;
+    rq.nshards = req->nshards ? req->nshards : 1;
+    rq.stop_above = req->stop_above;
+    rq.budget_s = req->time_budget_s;
+    return run_req(c, rq, out);
+}
+
+int simba_synthesize(simba_ctx *c, int size_bound, int shuffled, double time_budget_s, simba_outcome *out)
+{
+    if (!c)
+        return fail(SIMBA_EINVAL, "null context");
+    memset(out, 0, sizeof(*out));
+    out->rank = SIMBA_NO_RANK;
+    if (size_bound < 1)
+        return fail(SIMBA_EINVAL, "size bound must be >= 1, got %d", size_bound);
+    if (size_bound > c->max_size)
+        return fail(SIMBA_EINVAL, "size bound %d exceeds table extent %d", size_bound, c->max_size);
+    using clk = std::chrono::steady_clock;
+    const bool has_budget = time_budget_s >= 0;
+    const auto deadline = clk::now() + std::chrono::duration_cast<clk::duration>(
+                                           std::chrono::duration<double>(has_budget ? time_budget_s : 0));
+    auto remaining = [&]() {
+        return has_budget ? std::chrono::duration<double>(deadline - clk::now()).count() : -1.0;
+    };
+    for (int s = 1; s <= size_bound; ++s) {
+        const auto t0 = clk::now();
+        simba_result r{};
+        uint64_t visited = 0;
+        bool hit = false, stopped = false;
+        if (!shuffled) {
+            Req rq{};
+            rq.size = s;
+            rq.mode = SIMBA_MODE_SEARCH;
+            rq.lo = 0;
+            rq.hi = row_total(c, s);
+            rq.nshards = 1;
+            rq.stop_above = SIMBA_NO_RANK;
+            rq.budget_s = has_budget ? std::max(0.0, remaining()) : -1.0;
+            int rc = run_req(c, rq, &r);
+            if (rc)
+                return rc;
+            out->kernel_ms += r.kernel_ms;
+            out->launches += r.launches;
+            visited = r.visited;
+            hit = r.found;
+            stopped = !r.completed;
+        } else {
+            // engine.py:222-262 in shuffled mode: every operator block is
+            // scanned in full in permuted order; the block minimum is kept.
+            std::vector<std::pair<uint64_t, uint64_t>> blocks;
+            if (s == 1) {
+                blocks.push_back({0, (uint64_t)c->k});
+            } else {
+                uint64_t off = 0;
+                for (int op = 0; op < 8; ++op) {
+                    const uint64_t cnt = (uint64_t)c->rows[s][op];
+                    if (cnt)
+                        blocks.push_back({off, cnt});
+                    off += cnt;
+                }
+            }
+            for (auto &b : blocks) {
+                Req rq{};
+                rq.size = s;
+                rq.mode = SIMBA_MODE_SEARCH;
+                rq.shuffled = true;
+                rq.lo = 0;
+                rq.hi = b.second;
+                rq.offset = b.first;
+                rq.block_total = b.second;
+                rq.nshards = 1;
+                rq.stop_above = SIMBA_NO_RANK;
+                rq.budget_s = has_budget ? std::max(0.0, remaining()) : -1.0;
+                int rc = run_req(c, rq, &r);
+                if (rc)
+                    return rc;
+                out->kernel_ms += r.kernel_ms;
+                out->launches += r.launches;
+                visited += r.visited;
+                if (r.found) {
+                    hit = true;
+                    break;
+                }
+                if (!r.completed) {
+                    stopped = true;
+                    break;
+                }
+            }
+        }
+        out->visited[s - 1] = visited;
+        out->millis[s - 1] = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+        out->nsizes = s;
+        if (hit) {
+            out->status = SIMBA_STATUS_FOUND;
+            out->size = s;
+            out->rank = r.best_rank;
+            memcpy(out->tokens, r.tokens, sizeof(out->tokens));
+            return SIMBA_OK;
+        }
+        if (stopped || (has_budget && remaining() < 0)) {
+            out->status = SIMBA_STATUS_TIMED_OUT;
+            return SIMBA_OK;
+        }
+    }
+    out->status = SIMBA_STATUS_NOT_FOUND;
+    return SIMBA_OK;
+}
+
+int simba_decode(simba_ctx *c, uint64_t rank, int size, int32_t *tokens)
+{
+    if (!c)
+        return fail(SIMBA_EINVAL, "null context");
+    if (size < 1 || size > c->max_size)
+        return fail(SIMBA_ERANGE, "size %d outside table extent 1..%d", size, c->max_size);
+    if (rank >= row_total(c, size))
+        return fail(SIMBA_ERANGE, "rank %llu out of range for size %d (total %llu)", (unsigned long long)rank,
+                    size, (unsigned long long)row_total(c, size));
+    CK(cudaSetDevice(c->device));
+    return decode_rank(c, rank, size, tokens);
+}
+
+}  // extern "C"
