@@ -65,7 +65,8 @@ typedef struct simba_ctx simba_ctx;
 
 typedef struct {
     int device;          /* CUDA ordinal (default 0) */
-    int r0;              /* super-leaf size cutoff; 0 = auto */
+    int r0;              /* shared-memory value-table cutoff (lane digit); 0 = auto */
+    int rg;              /* global value-table cutoff (left values, siblings); 0 = auto */
     int table_examples;  /* examples with value tables (1, 2 or 4); 0 = auto */
     int block_threads;   /* 0 = auto (256) */
     int blocks_per_sm;   /* 0 = occupancy calculator */
@@ -150,9 +151,9 @@ int simba_synthesize(simba_ctx *ctx, int size_bound, int shuffled, double time_b
 /* codec.decode(rank, size, table) (codec.py:136-144) on the device. */
 int simba_decode(simba_ctx *ctx, uint64_t rank, int size, int32_t *tokens);
 
-/* Effective configuration of a context (for reports): r0, table examples,
- * word bytes, grid blocks, block threads, shared-memory bytes per block. */
-int simba_ctx_info(simba_ctx *ctx, int *r0, int *table_examples, int *word_bytes, int *grid_blocks,
+/* Effective configuration of a context (for reports): r0, rg, table
+ * examples, word bytes, grid blocks, block threads, shared-memory bytes per block. */
+int simba_ctx_info(simba_ctx *ctx, int *r0, int *rg, int *table_examples, int *word_bytes, int *grid_blocks,
                    int *block_threads, int *smem_bytes);
 
 const char *simba_last_error(void);

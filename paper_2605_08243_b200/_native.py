@@ -26,6 +26,7 @@ class Options(C.Structure):
     _fields_ = [
         ("device", C.c_int),
         ("r0", C.c_int),
+        ("rg", C.c_int),
         ("table_examples", C.c_int),
         ("block_threads", C.c_int),
         ("blocks_per_sm", C.c_int),
@@ -90,7 +91,7 @@ SIGNATURES = {
     "simba_run": (C.c_int, [C.c_void_p, C.POINTER(Range), C.POINTER(Result)]),
     "simba_synthesize": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_double, C.POINTER(Outcome)]),
     "simba_decode": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
-    "simba_ctx_info": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int)] * 6),
+    "simba_ctx_info": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int)] * 7),
     "simba_last_error": (C.c_char_p, []),
     "simba_device_count": (C.c_int, []),
     "simba_launch_count": (C.c_uint64, []),

@@ -38,7 +38,7 @@ def _decoder(table: CountTable):
     if ctx is None:
         # tables only; the (single, all-zero) example is never evaluated here
         spec = Specification(k=table.k, w=64, pairs=(((0,) * table.k, 0),))
-        ctx = DeviceContext(spec, min(table.max_size, 24), table_examples=1, r0=1)
+        ctx = DeviceContext(spec, min(table.max_size, 24), table_examples=1, r0=1, rg=1)
         _DECODERS[key] = ctx
     return ctx
 

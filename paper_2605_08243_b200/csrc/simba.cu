@@ -209,7 +209,7 @@ __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const O
                                      uint32_t R2, uint32_t off1, uint32_t off2, bool hit, uint32_t d1, uint32_t d2,
                                      uint64_t &my_count)
 {
-    const W *tbl = reinterpret_cast<const W *>(st.tbl);
+    const W *gtbl = reinterpret_cast<const W *>(p.gtbl);
     const W *ys = reinterpret_cast<const W *>(st.ys);
     const W mask = (W)p.mask;
 #pragma unroll
@@ -218,7 +218,7 @@ __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const O
         bcast_seg_array<W, MAXSO>(od.so, e, so);
         bcast_seg_array<W, MAXSL>(od.sl, e, sl);
         if (hit) {
-            const W *te = tbl + (size_t)e * p.tbl_len;
+            const W *te = gtbl + (size_t)e * p.gtbl_len;
             W vX = (W)0;
             if constexpr (POP != OP_NONE)
                 vX = segs_apply(sl, te[off1 + d1]);
@@ -242,24 +242,31 @@ template <class W, int E, int POP, int NSO, int NSL>
 __device__ __forceinline__ void sweep_unit(const KParams &p, const Staged &st, const Odometer<W, E> &od,
                                            const Seg<W> (&so)[MAXSO], const Seg<W> (&sl)[MAXSL], W y0, W mask,
                                            uint64_t ubase, uint32_t R2, uint32_t off1, uint32_t off2,
-                                           uint32_t d1s, uint32_t d2s, uint32_t u0, uint32_t u1, int lane,
+                                           uint32_t d1s, uint32_t d2s, uint64_t u0, uint64_t u1, int lane,
                                            uint64_t &my_count)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));  // example-0 value table
+    const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));  // example 0, sizes <= R0 (LDS)
+    const W *g0 = reinterpret_cast<const W *>(p.gtbl);               // example 0, sizes <= RG (global)
     auto value = [&](W vX, W vR) -> W { return segs_first<W, NSO>(so, apply_bin_t<W, POP>(vX, vR)); };
     auto miss = [&](W v) -> bool { return ((v ^ y0) & mask) != 0; };
     if (R2 >= 32) {
         // lanes over d2, d1 warp-uniform (vX hoisted per row)
         uint32_t dlo = d2s;
+        W gnext = (W)0;
+        if constexpr (POP != OP_NONE)
+            gnext = g0[off1 + d1s];
         for (uint32_t d1 = d1s;; ++d1, dlo = 0) {
-            const uint32_t row = d1 * R2;
+            const uint64_t row = (uint64_t)d1 * R2;
             if (row >= u1)
                 break;
-            const uint32_t dhi = min(R2, u1 - row);
+            const uint32_t dhi = (uint32_t)min((uint64_t)R2, u1 - row);
             W vX = (W)0;
-            if constexpr (POP != OP_NONE)
-                vX = segs_first<W, NSL>(sl, t0[off1 + d1]);
+            if constexpr (POP != OP_NONE) {
+                vX = segs_first<W, NSL>(sl, gnext);
+                if (row + R2 < u1)
+                    gnext = g0[off1 + d1 + 1];  // prefetch the next row's left value
+            }
             const W *tr = t0 + off2 + lane;
             uint32_t it = dlo;
             for (; it + 128 <= dhi; it += 128) {
@@ -290,15 +297,17 @@ __device__ __forceinline__ void sweep_unit(const KParams &p, const Staged &st, c
         const uint32_t ld2 = (uint32_t)lane - lg * R2;
         const bool lane_ok = lg < G;
         const W vR = t0[off2 + (lane_ok ? ld2 : 0)];
-        for (uint32_t d1b = d1s; d1b * R2 < u1; d1b += 2 * G) {
+        for (uint32_t d1b = d1s; (uint64_t)d1b * R2 < u1; d1b += 2 * G) {
             const uint32_t da = d1b + lg, db = d1b + G + lg;
             const uint32_t ua = da * R2 + ld2, ub = db * R2 + ld2;
             const bool acta = lane_ok && ua >= u0 && ua < u1;
             const bool actb = lane_ok && ub >= u0 && ub < u1;
             W xa = (W)0, xb = (W)0;
             if constexpr (POP != OP_NONE) {
-                xa = segs_first<W, NSL>(sl, t0[off1 + (acta ? da : d1s)]);
-                xb = segs_first<W, NSL>(sl, t0[off1 + (actb ? db : d1s)]);
+                const W ga = g0[off1 + (acta ? da : d1s)];
+                const W gb = g0[off1 + (actb ? db : d1s)];
+                xa = segs_first<W, NSL>(sl, ga);
+                xb = segs_first<W, NSL>(sl, gb);
             }
             const bool ha = acta && !miss(value(xa, vR));
             const bool hb = actb && !miss(value(xb, vR));
@@ -359,9 +368,10 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
             if (!od.have_x || q >= od.qend)
                 od.decode_x(q);
             const uint64_t qb = od.qb;
-            const uint32_t R1 = (uint32_t)t->T[od.sz1], off1 = t->toff[od.sz1];
+            const uint64_t R1 = t->T[od.sz1];
+            const uint32_t off1 = t->toff[od.sz1];
             const uint64_t ubase = pb + qb * R2;
-            const uint64_t stop = min(ubase + (uint64_t)R1 * R2, n1);
+            const uint64_t stop = min(ubase + R1 * R2, n1);
             ++ss.units;
             if (od.ovf_l) {
                 ++ss.rank_units;
@@ -374,7 +384,7 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
                 } else {
                     bcast_seg_array<W, MAXSL>(od.sl, 0, sl);
                 }
-                const uint32_t u0 = (uint32_t)(n - ubase), u1 = (uint32_t)(stop - ubase);
+                const uint64_t u0 = n - ubase, u1 = stop - ubase;
                 const uint32_t d1s = (uint32_t)(q - qb);
                 if (od.nsl == 0)
                     sweep_unit<W, E, POP, NSO, 0>(p, st, od, so, sl, y0, mask, ubase, R2, off1, off2, d1s, d2s, u0,
@@ -511,8 +521,9 @@ __global__ void __launch_bounds__(256, 2) unit_kernel(const __grid_constant__ KP
     Odometer<W, E> od;
     od.L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
     od.t = st.t;
-    od.tbl_e = reinterpret_cast<const W *>(st.tbl) + (size_t)(lane & (E - 1)) * p.tbl_len;
+    od.gt_e = reinterpret_cast<const W *>(p.gtbl) + (size_t)(lane & (E - 1)) * p.gtbl_len;
     od.R0 = p.R0;
+    od.RG = p.RG;
     od.s = p.s;
     od.lane = lane;
     od.ex = lane & (E - 1);
@@ -591,7 +602,7 @@ __global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ KPa
 
 
 template <class W>
-__global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int R0, int E, uint32_t tbl_len, W *out)
+__global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int RG, int E, uint32_t tbl_len, W *out)
 {
     const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (uint32_t)E * tbl_len)
@@ -599,7 +610,7 @@ __global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int R0, 
     const uint32_t e = idx / tbl_len;
     const uint32_t j = idx - e * tbl_len;
     int sz = 1;
-    while (sz < R0 && tabs->toff[sz + 1] <= j)
+    while (sz < RG && tabs->toff[sz + 1] <= j)
         ++sz;
     int8_t buf[MAXS];
     decode_tokens(tabs, j - tabs->toff[sz], sz, buf);
@@ -683,8 +694,9 @@ int build_rows(int k, int max_size, std::vector<std::array<u128, 9>> &rows, int 
 
 struct simba_ctx {
     int device = 0, k = 0, w = 0, n = 0, max_size = 0;
-    int wbytes = 4, R0 = 1, E = 1, kernel = 0;
-    uint32_t tbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
+    int wbytes = 4, R0 = 1, RG = 1, E = 1, kernel = 0;
+    uint32_t tbl_len = 0, gtbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
+    unsigned char *d_gtbl = nullptr;
     int block_threads = 256, grid_unit = 0, grid_direct = 0;
     int smem_unit = 0, smem_direct = 0;
     uint32_t lvl_off = 0;
@@ -729,13 +741,16 @@ int setup_kernels(simba_ctx *c)
 template <class W>
 int build_value_tables(simba_ctx *c)
 {
-    const uint32_t total = (uint32_t)c->E * c->tbl_len;
+    const uint32_t total = (uint32_t)c->E * c->gtbl_len;
     const int bt = 128;
     value_table_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(
-        c->d_tabs, reinterpret_cast<const W *>(c->d_blob + c->tbl_bytes), c->k, c->R0, c->E, c->tbl_len,
-        reinterpret_cast<W *>(c->d_blob));
+        c->d_tabs, reinterpret_cast<const W *>(c->d_blob + c->tbl_bytes), c->k, c->RG, c->E, c->gtbl_len,
+        reinterpret_cast<W *>(c->d_gtbl));
     g_launches++;
     CK(cudaGetLastError());
+    // shared-memory copy: example 0, sizes <= R0 (a prefix of the global table)
+    CK(cudaMemcpyAsync(c->d_blob, c->d_gtbl, (size_t)c->tbl_len * sizeof(W), cudaMemcpyDeviceToDevice,
+                       c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return SIMBA_OK;
 }
@@ -832,6 +847,9 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.tabs = c->d_tabs;
     p.tbl = c->d_blob;
     p.tbl_len = c->tbl_len;
+    p.gtbl = c->d_gtbl;
+    p.gtbl_len = c->gtbl_len;
+    p.RG = c->RG;
     p.k = c->k;
     p.n = c->n;
     p.s = rq.size;
@@ -1040,20 +1058,20 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     while (E > n)
         E >>= 1;
     c->E = E;
-    // super-leaf cut-off: largest R0 whose E value tables fit the budget and
-    // whose per-size counts keep unit-local indices in 32 bits
-    const uint64_t budget = 64 * 1024;
-    int R0 = o.r0;
+    // Value tables (per spec, memory independent of the search size):
+    //   shared: example 0, every subtree of size <= R0 (the lane-varying digit)
+    //   global: E examples, every subtree of size <= RG (left values, siblings)
     auto tbl_size = [&](int r) {
         uint64_t s = 0;
         for (int z = 1; z <= r; ++z)
             s += t.T[z];
         return s;
     };
+    int R0 = o.r0;
     if (R0 == 0) {
         R0 = 1;
         for (int r = 2; r <= max_size; ++r) {
-            if (t.T[r] > 65535 || tbl_size(r) * E * c->wbytes > budget)
+            if (t.T[r] > 65535 || tbl_size(r) * c->wbytes > 64 * 1024)
                 break;
             R0 = r;
         }
@@ -1063,21 +1081,42 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         for (int r = 1; r <= R0; ++r)
             if (t.T[r] > 65535)
                 return bail(fail(SIMBA_EINVAL, "r0 %d: T[%d] exceeds 65535", R0, r));
-        if (tbl_size(R0) * E * c->wbytes > 200 * 1024)
-            return bail(fail(SIMBA_EINVAL, "r0 %d: value tables exceed shared memory", R0));
+        if (tbl_size(R0) * c->wbytes > 160 * 1024)
+            return bail(fail(SIMBA_EINVAL, "r0 %d: value table exceeds shared memory", R0));
+    }
+    int RG = o.rg;
+    if (RG == 0) {
+        // largest RG whose tables stay small against the search itself
+        // (<= 16M entries, <= 1/16 of all candidates up to max_size)
+        const uint64_t cap = std::max<uint64_t>(tbl_size(R0), tbl_size(max_size) / 16);
+        RG = R0;
+        for (int r = R0 + 1; r <= max_size - 2; ++r) {
+            if (t.T[r] >= (1ull << 27) || tbl_size(r) > (16ull << 20) || tbl_size(r) > cap)
+                break;
+            RG = r;
+        }
+    } else {
+        if (RG < R0 || RG > max_size)
+            return bail(fail(SIMBA_EINVAL, "rg %d outside %d..%d", RG, R0, max_size));
+        if (t.T[RG] >= (1ull << 27) || tbl_size(RG) * E > (64ull << 20))
+            return bail(fail(SIMBA_EINVAL, "rg %d: global value table too large", RG));
     }
     c->R0 = R0;
+    c->RG = RG;
     {
-        uint32_t off = 0;
+        uint32_t off = 0, soff = 0;
         for (int z = 1; z <= MAXS; ++z) {
             t.toff[z] = off;
-            if (z <= R0)
+            if (z <= RG)
                 off += (uint32_t)t.T[z];
+            if (z <= R0)
+                soff += (uint32_t)t.T[z];
         }
-        c->tbl_len = off;
+        c->gtbl_len = off;
+        c->tbl_len = soff;
     }
     auto pad16 = [](uint64_t b) { return (uint32_t)((b + 15) & ~15ull); };
-    c->tbl_bytes = pad16((uint64_t)E * c->tbl_len * c->wbytes);
+    c->tbl_bytes = pad16((uint64_t)c->tbl_len * c->wbytes);
     c->ex_bytes = pad16((uint64_t)n * (k + 1) * c->wbytes);
     c->stage_examples = c->ex_bytes <= 32 * 1024;
     c->block_threads = o.block_threads ? o.block_threads : 256;
@@ -1117,6 +1156,8 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         return cuda_bail(e, "cudaMalloc(tabs)");
     if ((e = cudaMalloc(&c->d_blob, (size_t)c->tbl_bytes + c->ex_bytes)) != cudaSuccess)
         return cuda_bail(e, "cudaMalloc(blob)");
+    if ((e = cudaMalloc(&c->d_gtbl, (size_t)c->E * c->gtbl_len * c->wbytes + 16)) != cudaSuccess)
+        return cuda_bail(e, "cudaMalloc(global value table)");
     if ((e = cudaMalloc(&c->d_ctr, sizeof(unsigned long long) * kCtrWords)) != cudaSuccess)
         return cuda_bail(e, "cudaMalloc(counters)");
     if ((e = cudaMalloc(&c->d_tok, sizeof(int32_t) * MAXS)) != cudaSuccess)
@@ -1173,6 +1214,8 @@ void simba_ctx_destroy(simba_ctx *c)
         cudaFree(c->d_tabs);
     if (c->d_blob)
         cudaFree(c->d_blob);
+    if (c->d_gtbl)
+        cudaFree(c->d_gtbl);
     if (c->d_ctr)
         cudaFree(c->d_ctr);
     if (c->d_tok)
@@ -1188,13 +1231,15 @@ void simba_ctx_destroy(simba_ctx *c)
     delete c;
 }
 
-int simba_ctx_info(simba_ctx *c, int *r0, int *table_examples, int *word_bytes, int *grid_blocks,
+int simba_ctx_info(simba_ctx *c, int *r0, int *rg, int *table_examples, int *word_bytes, int *grid_blocks,
                    int *block_threads, int *smem_bytes)
 {
     if (!c)
         return fail(SIMBA_EINVAL, "null context");
     if (r0)
         *r0 = c->R0;
+    if (rg)
+        *rg = c->RG;
     if (table_examples)
         *table_examples = c->E;
     if (word_bytes)

@@ -26,7 +26,7 @@ struct __align__(16) Tabs {
     uint64_t T[MAXS + 1];                 // T[s][8]
     uint64_t m64[MAXS + 1];               // 64-bit magic for division by T[s]
     uint32_t m32[MAXS + 1];               // 32-bit magic (valid when T[s] < 2^32)
-    uint32_t toff[MAXS + 1];              // value-table offset of size s (s <= R0)
+    uint32_t toff[MAXS + 1];              // value-table offset of size s (s <= RG)
     uint8_t sh1[MAXS + 1];
     uint8_t sh2[MAXS + 1];
     uint8_t pad_[6];
@@ -36,11 +36,13 @@ struct __align__(16) Tabs {
 
 struct KParams {
     const Tabs *tabs;        // global copy of the tables
-    const void *tbl;         // [E][tbl_len] super-leaf values (word type W)
+    const void *tbl;         // unused (kept for layout); see gtbl / shared copy
+    const void *gtbl;        // [E][gtbl_len] values of every subtree of size <= RG (global)
     const uint64_t *X;       // [n][k] inputs
     const uint64_t *Y;       // [n] outputs
-    uint32_t tbl_len;
-    int k, n, s, R0, E;
+    uint32_t tbl_len;        // entries of sizes <= R0 (shared-memory copy, example 0)
+    uint32_t gtbl_len;       // entries of sizes <= RG per example (global)
+    int k, n, s, R0, RG, E;
     int mode;                // SIMBA_MODE_*
     int shuffled;
     uint64_t mask;
@@ -327,8 +329,8 @@ __device__ __forceinline__ W segs_apply(const Seg<W> (&s)[N], W v)
 // ---------------------------------------------------------------------------
 
 // Value of the size-sz expression of rank r on this lane's example: unrank as
-// codec.py:89-133 but stop at subtrees of size <= R0, whose values come from
-// the per-spec value table (tbl_e[toff[size] + rank]).  Post-order folding on
+// codec.py:89-133 but stop at subtrees of size <= R0 (the cut-off argument),
+// whose values come from the per-spec value table (tbl_e[toff[size] + rank]).  Post-order folding on
 // an explicit frame stack; control flow depends on (sz, r) only.
 template <class W>
 __device__ __noinline__ W eval_subtree(const Tabs *t, const W *tbl_e, int R0, int sz, uint64_t r)
@@ -434,8 +436,8 @@ template <class W, int E>
 struct Odometer {
     WarpLevels<W, E> *L;   // this warp's shared-memory levels
     const Tabs *t;
-    const W *tbl_e;        // this lane's example table
-    int R0, s, lane, ex;
+    const W *gt_e;         // this lane's example: values of all subtrees of size <= RG
+    int R0, RG, s, lane, ex;
     // outer state
     int no;                // valid outer levels
     bool have_outer;
@@ -460,9 +462,9 @@ struct Odometer {
 
     __device__ __forceinline__ W sib_value(int j, uint64_t q) const
     {
-        if (j <= R0)
-            return tbl_e[t->toff[j] + (uint32_t)q];
-        return eval_subtree<W>(t, tbl_e, R0, j, q);
+        if (j <= RG)
+            return gt_e[t->toff[j] + (uint32_t)q];
+        return eval_subtree<W>(t, gt_e, RG, j, q);
     }
 
     template <int CAP>
@@ -551,7 +553,7 @@ struct Odometer {
     __device__ __noinline__ void decode_x(uint64_t q)
     {
         LevelStack<W, E> &st = L->xs;
-        if (pj <= R0) {
+        if (pj <= RG) {
             sz1 = pj;
             qb = 0;
             qend = t->T[pj];
@@ -566,7 +568,7 @@ struct Odometer {
             int sz = (nx == 0) ? pj : st.csz[nx - 1];
             const uint64_t rb = (nx == 0) ? 0 : st.end[nx - 1] - t->T[sz];
             uint64_t r = q - rb;
-            while (sz > R0) {
+            while (sz > RG) {
                 const int op = find_slot(t, sz, r);
                 if (op == OP_NOT || op == OP_NEG) {
                     push_level(st, nx++, op, sz - 1, q - r + t->T[sz - 1], (W)0);

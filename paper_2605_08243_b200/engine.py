@@ -88,6 +88,7 @@ class EngineConfig:
     time_budget: float | None = None
     device: int = 0
     r0: int = 0
+    rg: int = 0
     table_examples: int = 0
     kernel: str = "unit"
 
@@ -157,12 +158,12 @@ class DeviceContext:
     """A Specification bound to one GPU: tables, examples and the per-spec
     super-leaf value tables staged in device memory (simba_ctx_create)."""
 
-    def __init__(self, spec: Specification, max_size: int, device: int = 0, r0: int = 0,
+    def __init__(self, spec: Specification, max_size: int, device: int = 0, r0: int = 0, rg: int = 0,
                  table_examples: int = 0, kernel: str = "unit", block_threads: int = 0,
                  blocks_per_sm: int = 0):
         self.spec = spec
         self.max_size = max_size
-        opts = N.Options(device=device, r0=r0, table_examples=table_examples,
+        opts = N.Options(device=device, r0=r0, rg=rg, table_examples=table_examples,
                          block_threads=block_threads, blocks_per_sm=blocks_per_sm,
                          kernel=_KERNELS[kernel])
         xs, ys = _spec_arrays(spec)
@@ -188,9 +189,9 @@ class DeviceContext:
         self.close()
 
     def info(self) -> dict:
-        vals = [C.c_int() for _ in range(6)]
+        vals = [C.c_int() for _ in range(7)]
         N.check_rc(N.lib.simba_ctx_info(self._ptr, *[C.byref(v) for v in vals]))
-        keys = ("r0", "table_examples", "word_bytes", "grid_blocks", "block_threads", "smem_bytes")
+        keys = ("r0", "rg", "table_examples", "word_bytes", "grid_blocks", "block_threads", "smem_bytes")
         return dict(zip(keys, (v.value for v in vals)))
 
     @staticmethod
@@ -252,7 +253,7 @@ def _check_args(spec: Specification, table: CountTable, cfg: EngineConfig):
 def synthesize(spec: Specification, table: CountTable, cfg: EngineConfig) -> SynthesisOutcome:
     """engine.synthesize (engine.py:190-276) on the device."""
     _check_args(spec, table, cfg)
-    with DeviceContext(spec, cfg.size_bound, device=cfg.device, r0=cfg.r0,
+    with DeviceContext(spec, cfg.size_bound, device=cfg.device, r0=cfg.r0, rg=cfg.rg,
                        table_examples=cfg.table_examples, kernel=cfg.kernel) as ctx:
         out = ctx.synthesize_raw(cfg.size_bound, shuffled=(cfg.mode == "shuffled"),
                                  time_budget=cfg.time_budget)
@@ -273,7 +274,7 @@ def count_solutions(spec: Specification, table: CountTable, cfg: EngineConfig) -
     engine.py:279-293, expr.py:201-218)."""
     _check_args(spec, table, cfg)
     out = []
-    with DeviceContext(spec, cfg.size_bound, device=cfg.device, r0=cfg.r0,
+    with DeviceContext(spec, cfg.size_bound, device=cfg.device, r0=cfg.r0, rg=cfg.rg,
                        table_examples=cfg.table_examples, kernel=cfg.kernel) as ctx:
         for s in range(1, cfg.size_bound + 1):
             t0 = time.perf_counter()

@@ -138,8 +138,9 @@ def test_exhaustive_counts_match_reference(name):
     assert [c.candidates for c in got] == [table.total(s) for s in range(1, C + 1)]
 
 
-@pytest.mark.parametrize("variant", [dict(r0=1), dict(r0=2), dict(r0=3, table_examples=1),
-                                     dict(table_examples=2), dict(table_examples=4), dict(kernel="direct")])
+@pytest.mark.parametrize("variant", [dict(r0=1, rg=1), dict(r0=2), dict(r0=2, rg=3), dict(r0=3, table_examples=1),
+                                     dict(r0=3, rg=6), dict(table_examples=2), dict(table_examples=4),
+                                     dict(kernel="direct")])
 def test_counts_independent_of_kernel_configuration(variant):
     for name in ("dense_k3_w3_n2", "C4_stress_i0", "dense_k3_w64_stress", "C2_s5_i0"):
         r = [r for r in load_golden("counts") if r["name"] == name][0]
@@ -152,11 +153,15 @@ def test_counts_independent_of_kernel_configuration(variant):
 # ---------------------------------------------------------------- rank windows (C5 sizes 11..13)
 
 
+# exercise both a large global table and the minimal one on the C5 windows
+WINDOW_RG = {"C5_s12_t1": 5, "C5dense_s13_op2": 5, "C5dense_s12_op4": 9, "C5_s13_t0": 9}
+
+
 @pytest.mark.parametrize("name", [r["name"] for r in load_golden("windows")])
 def test_windows_match_reference(name):
     r = [r for r in load_golden("windows") if r["name"] == name][0]
     spec = spec_of(r["spec"])
-    with DeviceContext(spec, r["size_bound"]) as ctx:
+    with DeviceContext(spec, r["size_bound"], rg=WINDOW_RG.get(r["name"], 0)) as ctx:
         c = ctx.count(r["size"], r["lo"], r["hi"])
         assert (c.count, c.best_rank) == (r["count"], r["first"])
         assert c.visited == r["hi"] - r["lo"]
