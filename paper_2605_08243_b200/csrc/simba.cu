@@ -178,6 +178,14 @@ __device__ __noinline__ bool full_check(const KParams &p, const Staged &st, uint
 // ===========================================================================
 // unit sweep
 // ===========================================================================
+//
+// Every candidate of a unit is  v = CHAIN(table value)  where CHAIN is a short
+// list of (LOP3, IMAD) segments: in variant A (lanes over the last digit d2,
+// R2 >= 32) the chain is P(vX, .) followed by the outer ancestors, rebuilt per
+// row d1 (only its first segment changes); in variant B (R2 < 32, lanes over
+// (d1, d2) pairs) it is LEFT, P(., vR), OUTER per lane, with the lane's fixed
+// right value vR folded in.  The loop bodies are generic in the operators:
+// one instantiation per chain length.
 
 template <class W, int N>
 __device__ __forceinline__ void bcast_seg_array(const Seg<W> (&in)[N], int src, Seg<W> (&out)[N])
@@ -191,23 +199,14 @@ __device__ __forceinline__ void bcast_seg_array(const Seg<W> (&in)[N], int src, 
     }
 }
 
-template <class W, int N, int M>
-__device__ __forceinline__ W segs_first(const Seg<W> (&s)[M], W v)
-{
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-        v = seg_apply(s[i], v);
-    return v;
-}
-
 // Rare path: at least one lane matched example 0 through the tables.  Refine
 // on examples 1..E-1 (their segments live in lanes 1..E-1 of the odometer),
 // then verify the survivors against every example with the reference-exact
 // evaluator (decode_tokens + eval_rpn).
-template <class W, int E, int POP>
-__device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const Odometer<W, E> &od, uint64_t ubase,
-                                     uint32_t R2, uint32_t off1, uint32_t off2, bool hit, uint32_t d1, uint32_t d2,
-                                     uint64_t &my_count)
+template <class W, int E>
+__device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
+                                     uint64_t ubase, uint32_t R2, uint32_t off1, uint32_t off2, bool hit,
+                                     uint32_t d1, uint32_t d2, uint64_t &my_count)
 {
     const W *gtbl = reinterpret_cast<const W *>(p.gtbl);
     const W *ys = reinterpret_cast<const W *>(st.ys);
@@ -219,10 +218,11 @@ __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const O
         bcast_seg_array<W, MAXSL>(od.sl, e, sl);
         if (hit) {
             const W *te = gtbl + (size_t)e * p.gtbl_len;
-            W vX = (W)0;
-            if constexpr (POP != OP_NONE)
-                vX = segs_apply(sl, te[off1 + d1]);
-            const W v = segs_apply(so, apply_bin_t<W, POP>(vX, te[off2 + d2]));
+            const W vR = te[off2 + d2];
+            W v = vR;
+            if (pop != OP_NONE)
+                v = apply_bin<W>(pop, segs_apply(sl, te[off1 + d1]), vR);
+            v = segs_apply(so, v);
             hit = (((v ^ ys[e]) & mask) == 0);
         }
     }
@@ -233,88 +233,141 @@ __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const O
     }
 }
 
-// Lane-parallel sweep of unit-local indices [u0, u1) (index = d1*R2 + d2) of
-// one unit whose first index decomposes as (d1s, d2s).  NSO / NSL: segments
-// the outer / left chains actually use (the rest are identities, skipped at
-// compile time).  Tables are read through the dynamic shared-memory symbol so
-// the compiler emits LDS.
-template <class W, int E, int POP, int NSO, int NSL>
-__device__ __forceinline__ void sweep_unit(const KParams &p, const Staged &st, const Odometer<W, E> &od,
-                                           const Seg<W> (&so)[MAXSO], const Seg<W> (&sl)[MAXSL], W y0, W mask,
-                                           uint64_t ubase, uint32_t R2, uint32_t off1, uint32_t off2,
-                                           uint32_t d1s, uint32_t d2s, uint64_t u0, uint64_t u1, int lane,
-                                           uint64_t &my_count)
+template <class W, int N>
+__device__ __forceinline__ W chain_apply(const Seg<W> (&c)[N], W v)
+{
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        v = seg_apply(c[i], v);
+    return v;
+}
+
+// How P(vX, .) joins the outer chain (uniform per P block).
+enum : int { PJ_NONE = 0, PJ_MERGE_BW = 1, PJ_MERGE_AFF = 2, PJ_SEPARATE = 3 };
+
+template <class W>
+__device__ __forceinline__ void pseg_left_fixed(int pop, W s, Seg<W> &g, bool &bitwise)
+{
+    g = seg_identity<W>();
+    bitwise = (pop == OP_AND || pop == OP_OR || pop == OP_XOR);
+    switch (pop) {
+    case OP_AND: g.m = s; break;
+    case OP_OR: g.m = ~s; g.x = s; break;
+    case OP_XOR: g.x = s; break;
+    case OP_ADD: g.b = s; break;
+    case OP_SUB: g.a = (W)~(W)0; g.b = s; break;
+    default: g.a = s; break;  // MUL
+    }
+}
+
+// first chain segment for a row with left value vX
+template <class W>
+__device__ __forceinline__ Seg<W> first_seg(int pj, int pop, W vX, const Seg<W> &so0)
+{
+    Seg<W> g;
+    bool bw;
+    pseg_left_fixed(pop, vX, g, bw);
+    if (pj == PJ_MERGE_BW) {  // so0's bitwise part after g's
+        Seg<W> r = so0;
+        r.m = g.m & so0.m;
+        r.x = (g.x & so0.m) ^ so0.x;
+        return r;
+    }
+    if (pj == PJ_MERGE_AFF) {  // so0 has no bitwise part: A0 after g
+        Seg<W> r = so0;
+        r.b = so0.a * g.b + so0.b;
+        r.a = so0.a * g.a;
+        return r;
+    }
+    return g;  // PJ_SEPARATE (or P absent: unused)
+}
+
+// Variant A: R2 >= 32, lanes over d2 (4 x 32 per step), d1 uniform per row.
+// c[0] is rebuilt per row from the row's left value; c[1..NT-1] are fixed.
+template <class W, int E, int NT>
+__device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop, int pj,
+                                     const Seg<W> &so0, const Seg<W> (&rest)[NT], const Seg<W> (&sl)[MAXSL], W y0,
+                                     uint64_t ubase, uint32_t R2, uint32_t off1, uint32_t off2, uint32_t d1s,
+                                     uint32_t d2s, uint64_t u1, int lane, uint64_t &my_count)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));  // example 0, sizes <= R0 (LDS)
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);               // example 0, sizes <= RG (global)
-    auto value = [&](W vX, W vR) -> W { return segs_first<W, NSO>(so, apply_bin_t<W, POP>(vX, vR)); };
-    auto miss = [&](W v) -> bool { return ((v ^ y0) & mask) != 0; };
-    if (R2 >= 32) {
-        // lanes over d2, d1 warp-uniform (vX hoisted per row)
-        uint32_t dlo = d2s;
-        W gnext = (W)0;
-        if constexpr (POP != OP_NONE)
-            gnext = g0[off1 + d1s];
-        for (uint32_t d1 = d1s;; ++d1, dlo = 0) {
-            const uint64_t row = (uint64_t)d1 * R2;
-            if (row >= u1)
-                break;
-            const uint32_t dhi = (uint32_t)min((uint64_t)R2, u1 - row);
-            W vX = (W)0;
-            if constexpr (POP != OP_NONE) {
-                vX = segs_first<W, NSL>(sl, gnext);
-                if (row + R2 < u1)
-                    gnext = g0[off1 + d1 + 1];  // prefetch the next row's left value
-            }
-            const W *tr = t0 + off2 + lane;
-            uint32_t it = dlo;
-            for (; it + 128 <= dhi; it += 128) {
-                const W v0 = value(vX, tr[it]);
-                const W v1 = value(vX, tr[it + 32]);
-                const W v2 = value(vX, tr[it + 64]);
-                const W v3 = value(vX, tr[it + 96]);
-                const bool m0 = miss(v0), m1 = miss(v1), m2 = miss(v2), m3 = miss(v3);
-                if (__any_sync(FULL, !(m0 && m1 && m2 && m3))) {
-                    on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, !m0, d1, it + lane, my_count);
-                    on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, !m1, d1, it + 32 + lane, my_count);
-                    on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, !m2, d1, it + 64 + lane, my_count);
-                    on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, !m3, d1, it + 96 + lane, my_count);
-                }
-            }
-            for (; it < dhi; it += 32) {
-                const uint32_t d2 = it + lane;
-                const bool act = d2 < dhi;
-                const bool hit = act && !miss(value(vX, t0[off2 + (act ? d2 : it)]));
-                if (__any_sync(FULL, hit))
-                    on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, hit, d1, d2, my_count);
+    const W mask = (W)p.mask;
+    Seg<W> c[NT];
+#pragma unroll
+    for (int i = 1; i < NT; ++i)
+        c[i] = rest[i];
+    c[0] = rest[0];
+    uint32_t dlo = d2s;
+    W gnext = (W)0;
+    if (pop != OP_NONE)
+        gnext = g0[off1 + d1s];
+    const W *tr = t0 + off2 + lane;
+    for (uint32_t d1 = d1s;; ++d1, dlo = 0) {
+        const uint64_t row = (uint64_t)d1 * R2;
+        if (row >= u1)
+            break;
+        const uint32_t dhi = (uint32_t)min((uint64_t)R2, u1 - row);
+        if (pop != OP_NONE) {
+            const W vX = segs_apply(sl, gnext);
+            if (row + R2 < u1)
+                gnext = g0[off1 + d1 + 1];  // prefetch the next row's left value
+            c[0] = first_seg(pj, pop, vX, so0);
+        }
+        for (uint32_t it = dlo; it < dhi; it += 128) {
+            // the shared table is padded by 128 words: reads past a row are harmless
+            const W v0 = chain_apply(c, tr[it]);
+            const W v1 = chain_apply(c, tr[it + 32]);
+            const W v2 = chain_apply(c, tr[it + 64]);
+            const W v3 = chain_apply(c, tr[it + 96]);
+            const uint32_t d2 = it + lane;
+            const bool h0 = d2 < dhi && ((v0 ^ y0) & mask) == 0;
+            const bool h1 = d2 + 32 < dhi && ((v1 ^ y0) & mask) == 0;
+            const bool h2 = d2 + 64 < dhi && ((v2 ^ y0) & mask) == 0;
+            const bool h3 = d2 + 96 < dhi && ((v3 ^ y0) & mask) == 0;
+            if (__any_sync(FULL, h0 || h1 || h2 || h3)) {
+                on_hits<W, E>(p, st, od, pop, ubase, R2, off1, off2, h0, d1, d2, my_count);
+                on_hits<W, E>(p, st, od, pop, ubase, R2, off1, off2, h1, d1, d2 + 32, my_count);
+                on_hits<W, E>(p, st, od, pop, ubase, R2, off1, off2, h2, d1, d2 + 64, my_count);
+                on_hits<W, E>(p, st, od, pop, ubase, R2, off1, off2, h3, d1, d2 + 96, my_count);
             }
         }
-    } else {
-        // R2 < 32: lanes over (d1, d2) pairs, G rows per step
-        const uint32_t G = 32u / R2;
-        const uint32_t lg = (uint32_t)lane / R2;
-        const uint32_t ld2 = (uint32_t)lane - lg * R2;
-        const bool lane_ok = lg < G;
-        const W vR = t0[off2 + (lane_ok ? ld2 : 0)];
-        for (uint32_t d1b = d1s; (uint64_t)d1b * R2 < u1; d1b += 2 * G) {
-            const uint32_t da = d1b + lg, db = d1b + G + lg;
-            const uint32_t ua = da * R2 + ld2, ub = db * R2 + ld2;
-            const bool acta = lane_ok && ua >= u0 && ua < u1;
-            const bool actb = lane_ok && ub >= u0 && ub < u1;
-            W xa = (W)0, xb = (W)0;
-            if constexpr (POP != OP_NONE) {
-                const W ga = g0[off1 + (acta ? da : d1s)];
-                const W gb = g0[off1 + (actb ? db : d1s)];
-                xa = segs_first<W, NSL>(sl, ga);
-                xb = segs_first<W, NSL>(sl, gb);
-            }
-            const bool ha = acta && !miss(value(xa, vR));
-            const bool hb = actb && !miss(value(xb, vR));
-            if (__any_sync(FULL, ha || hb)) {
-                on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, ha, acta ? da : 0, ld2, my_count);
-                on_hits<W, E, POP>(p, st, od, ubase, R2, off1, off2, hb, actb ? db : 0, ld2, my_count);
-            }
+    }
+}
+
+// Variant B: R2 < 32, lanes over (d1, d2) pairs (G = 32 / R2 rows per step,
+// 4 steps per iteration); the lane's chain LEFT, P(., vR), OUTER is fixed.
+template <class W, int E, int NT>
+__device__ __noinline__ void sweep_b(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
+                                     const Seg<W> (&c)[NT], W y0, uint64_t ubase, uint32_t R2, uint32_t off1,
+                                     uint32_t off2, uint32_t d1s, uint64_t u0, uint64_t u1, int lane,
+                                     uint64_t &my_count)
+{
+    const W *g0 = reinterpret_cast<const W *>(p.gtbl);
+    const W mask = (W)p.mask;
+    const uint32_t G = 32u / R2;
+    const uint32_t lg = (uint32_t)lane / R2;
+    const uint32_t ld2 = (uint32_t)lane - lg * R2;
+    const bool lane_ok = lg < G;
+    const W *rowp = g0 + off1;
+    const uint32_t d1e = (uint32_t)((u1 + R2 - 1) / R2);  // first row past the unit range
+    for (uint32_t d1b = d1s; d1b < d1e; d1b += 4 * G) {
+        bool h[4];
+        uint32_t d1v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t d1 = d1b + k * G + lg;
+            const uint64_t uu = (uint64_t)d1 * R2 + ld2;
+            const bool act = lane_ok && uu >= u0 && uu < u1;
+            const W v = chain_apply(c, rowp[act ? d1 : d1s]);
+            h[k] = act && ((v ^ y0) & mask) == 0;
+            d1v[k] = d1;
+        }
+        if (__any_sync(FULL, h[0] || h[1] || h[2] || h[3])) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                on_hits<W, E>(p, st, od, pop, ubase, R2, off1, off2, h[k], h[k] ? d1v[k] : 0, ld2, my_count);
         }
     }
 }
@@ -331,17 +384,46 @@ struct SweepStats {
     uint64_t count, units, rank_units;
 };
 
+template <class W, int E, int NT>
+__device__ __forceinline__ void dispatch_a_nt(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
+                                              int pj, const Seg<W> &so0, const Seg<W> (&chain)[8],
+                                              const Seg<W> (&sl)[MAXSL], W y0, uint64_t ubase, uint32_t R2,
+                                              uint32_t off1, uint32_t off2, uint32_t d1s, uint32_t d2s, uint64_t u1,
+                                              int lane, uint64_t &cnt)
+{
+    Seg<W> rest[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+        rest[i] = chain[i];
+    sweep_a<W, E, NT>(p, st, od, pop, pj, so0, rest, sl, y0, ubase, R2, off1, off2, d1s, d2s, u1, lane, cnt);
+}
+
+template <class W, int E, int NT>
+__device__ __forceinline__ void dispatch_b_nt(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
+                                              const Seg<W> (&chain)[8], W y0, uint64_t ubase, uint32_t R2,
+                                              uint32_t off1, uint32_t off2, uint32_t d1s, uint64_t u0, uint64_t u1,
+                                              int lane, uint64_t &cnt)
+{
+    Seg<W> c[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+        c[i] = chain[i];
+    sweep_b<W, E, NT>(p, st, od, pop, c, y0, ubase, R2, off1, off2, d1s, u0, u1, lane, cnt);
+}
+
 // All ranks [n, n1) of one P block (n1 <= pend).  The outer chain and P's
 // operator are fixed for the whole block; the X odometer advances unit by
-// unit inside this function, so consecutive units cost one decode_x step
-// (usually a single level) instead of a dispatch and a decode from the root.
-// Returns the first rank not scanned (n1 unless a search hit allows early exit).
-template <class W, int E, int POP, int NSO>
+// unit here, so consecutive units cost one decode_x step (usually a single
+// level).  Returns the first rank not scanned (n1 unless a search hit allows
+// early exit).
+template <class W, int E>
 __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, Odometer<W, E> &od, uint64_t n,
                                             uint64_t n1, int lane, SweepStats &ss)
 {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Tabs *t = stabs();
+    const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));
     const W y0 = reinterpret_cast<const W *>(st.ys)[0];
-    const W mask = (W)p.mask;
     Seg<W> so[MAXSO], sl[MAXSL];
     if constexpr (E == 1) {
 #pragma unroll
@@ -350,33 +432,65 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
     } else {
         bcast_seg_array<W, MAXSO>(od.so, 0, so);
     }
-    const Tabs *t = st.t;
-    const int prsz = od.prsz;
+    const int pop = od.pop, nso = od.nso, prsz = od.prsz;
     const uint32_t R2 = (uint32_t)t->T[prsz], off2 = t->toff[prsz];
     const uint64_t pb = od.pb;
-    if constexpr (POP == OP_NONE) {
-        ++ss.units;
-        sweep_unit<W, E, POP, NSO, 0>(p, st, od, so, sl, y0, mask, pb, R2, 0, off2, 0, (uint32_t)(n - pb),
-                                      (uint32_t)(n - pb), (uint32_t)(n1 - pb), lane, ss.count);
-        return n1;
+    const bool early = (p.mode == SIMBA_MODE_SEARCH);
+    // variant A chain layout: c[0] = first segment (per row), c[1..] = rest
+    int pj = PJ_NONE;
+    Seg<W> chainA[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        chainA[i] = seg_identity<W>();
+    int ntA = 1;
+    if (pop == OP_NONE) {
+#pragma unroll
+        for (int i = 0; i < MAXSO; ++i)
+            chainA[i] = so[i];
+        ntA = nso > 1 ? nso : 1;
     } else {
-        const bool early = (p.mode == SIMBA_MODE_SEARCH);
-        while (n < n1) {
+        const bool pbw = (pop == OP_AND || pop == OP_OR || pop == OP_XOR);
+        if (nso > 0 && (pbw || !od.so0_bw)) {
+            pj = pbw ? PJ_MERGE_BW : PJ_MERGE_AFF;
+#pragma unroll
+            for (int i = 0; i < MAXSO; ++i)
+                chainA[i] = so[i];  // chainA[0] replaced per row
+            ntA = nso;
+        } else {
+            pj = PJ_SEPARATE;
+#pragma unroll
+            for (int i = 0; i < MAXSO; ++i)
+                chainA[i + 1] = so[i];
+            ntA = nso + 1;
+        }
+    }
+    while (n < n1) {
+        uint64_t ubase, R1 = 1, stop;
+        uint32_t off1 = 0, d1s = 0, d2s;
+        if (pop == OP_NONE) {
+            ubase = pb;
+            d2s = (uint32_t)(n - pb);
+            stop = n1;
+            od.nsl = 0;
+            od.ovf_l = false;
+        } else {
             const uint64_t rel = n - pb;
             const uint64_t q = div_T(t, prsz, rel);
-            const uint32_t d2s = (uint32_t)(rel - q * R2);
+            d2s = (uint32_t)(rel - q * R2);
             if (!od.have_x || q >= od.qend)
                 od.decode_x(q);
-            const uint64_t qb = od.qb;
-            const uint64_t R1 = t->T[od.sz1];
-            const uint32_t off1 = t->toff[od.sz1];
-            const uint64_t ubase = pb + qb * R2;
-            const uint64_t stop = min(ubase + R1 * R2, n1);
-            ++ss.units;
-            if (od.ovf_l) {
-                ++ss.rank_units;
-                direct_range<W>(p, st, n, stop, false, ss.count);
-            } else {
+            R1 = t->T[od.sz1];
+            off1 = t->toff[od.sz1];
+            ubase = pb + od.qb * R2;
+            d1s = (uint32_t)(q - od.qb);
+            stop = min(ubase + R1 * R2, n1);
+        }
+        ++ss.units;
+        if (od.ovf_l) {
+            ++ss.rank_units;
+            direct_range<W>(p, st, n, stop, false, ss.count);
+        } else {
+            if (pop != OP_NONE) {
                 if constexpr (E == 1) {
 #pragma unroll
                     for (int i = 0; i < MAXSL; ++i)
@@ -384,49 +498,55 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
                 } else {
                     bcast_seg_array<W, MAXSL>(od.sl, 0, sl);
                 }
-                const uint64_t u0 = n - ubase, u1 = stop - ubase;
-                const uint32_t d1s = (uint32_t)(q - qb);
-                if (od.nsl == 0)
-                    sweep_unit<W, E, POP, NSO, 0>(p, st, od, so, sl, y0, mask, ubase, R2, off1, off2, d1s, d2s, u0,
-                                                  u1, lane, ss.count);
-                else
-                    sweep_unit<W, E, POP, NSO, MAXSL>(p, st, od, so, sl, y0, mask, ubase, R2, off1, off2, d1s, d2s,
-                                                      u0, u1, lane, ss.count);
             }
-            n = stop;
-            if (early && n < n1 && n > read_best(p))
-                break;  // everything left ranks above a hit
+            const uint64_t u0 = n - ubase, u1 = stop - ubase;
+            if (R2 >= 32) {
+                if (ntA <= 1)
+                    dispatch_a_nt<W, E, 1>(p, st, od, pop, pj, so[0], chainA, sl, y0, ubase, R2, off1, off2, d1s,
+                                           d2s, u1, lane, ss.count);
+                else if (ntA == 2)
+                    dispatch_a_nt<W, E, 2>(p, st, od, pop, pj, so[0], chainA, sl, y0, ubase, R2, off1, off2, d1s,
+                                           d2s, u1, lane, ss.count);
+                else if (ntA == 3)
+                    dispatch_a_nt<W, E, 3>(p, st, od, pop, pj, so[0], chainA, sl, y0, ubase, R2, off1, off2, d1s,
+                                           d2s, u1, lane, ss.count);
+                else
+                    dispatch_a_nt<W, E, 5>(p, st, od, pop, pj, so[0], chainA, sl, y0, ubase, R2, off1, off2, d1s,
+                                           d2s, u1, lane, ss.count);
+            } else {
+                // lane chain: LEFT, P(., vR), OUTER with vR = this lane's d2 value
+                const uint32_t lg = (uint32_t)lane / R2;
+                const uint32_t ld2 = (uint32_t)lane - lg * R2;
+                const W vR = t0[off2 + ld2];
+                SegChain<W, 8> ch;
+                ch.init();
+                if (pop != OP_NONE) {
+                    for (int i = 0; i < od.nsl; ++i)
+                        ch.then_seg(sl[i]);
+                    chain_right_fixed(ch, pop, vR);
+                } else {
+                    ch.then_affine((W)0, vR);  // value = vR whatever the row value
+                }
+                for (int i = 0; i < nso; ++i)
+                    ch.then_seg(so[i]);
+                int nt = ch.n;
+                nt = __reduce_max_sync(FULL, (unsigned)nt);
+                if (nt <= 2)
+                    dispatch_b_nt<W, E, 2>(p, st, od, pop, ch.s, y0, ubase, R2, off1, off2, d1s, u0, u1, lane,
+                                           ss.count);
+                else if (nt <= 4)
+                    dispatch_b_nt<W, E, 4>(p, st, od, pop, ch.s, y0, ubase, R2, off1, off2, d1s, u0, u1, lane,
+                                           ss.count);
+                else
+                    dispatch_b_nt<W, E, 8>(p, st, od, pop, ch.s, y0, ubase, R2, off1, off2, d1s, u0, u1, lane,
+                                           ss.count);
+            }
         }
-        return n;
+        n = stop;
+        if (early && n < n1 && n > read_best(p))
+            break;  // everything left ranks above a hit
     }
-}
-
-template <class W, int E, int POP>
-__device__ __forceinline__ uint64_t dispatch_nso(const KParams &p, const Staged &st, Odometer<W, E> &od, uint64_t n,
-                                                 uint64_t n1, int lane, SweepStats &ss)
-{
-    if (od.nso == 0)
-        return run_pblock<W, E, POP, 0>(p, st, od, n, n1, lane, ss);
-    if (od.nso == 1)
-        return run_pblock<W, E, POP, 1>(p, st, od, n, n1, lane, ss);
-    if (od.nso == 2)
-        return run_pblock<W, E, POP, 2>(p, st, od, n, n1, lane, ss);
-    return run_pblock<W, E, POP, 4>(p, st, od, n, n1, lane, ss);
-}
-
-template <class W, int E>
-__device__ __noinline__ uint64_t process_pblock(const KParams &p, const Staged &st, Odometer<W, E> &od, uint64_t n,
-                                                uint64_t n1, int lane, SweepStats &ss)
-{
-    switch (od.pop) {
-    case OP_AND: return dispatch_nso<W, E, OP_AND>(p, st, od, n, n1, lane, ss);
-    case OP_OR: return dispatch_nso<W, E, OP_OR>(p, st, od, n, n1, lane, ss);
-    case OP_XOR: return dispatch_nso<W, E, OP_XOR>(p, st, od, n, n1, lane, ss);
-    case OP_ADD: return dispatch_nso<W, E, OP_ADD>(p, st, od, n, n1, lane, ss);
-    case OP_SUB: return dispatch_nso<W, E, OP_SUB>(p, st, od, n, n1, lane, ss);
-    case OP_MUL: return dispatch_nso<W, E, OP_MUL>(p, st, od, n, n1, lane, ss);
-    default: return dispatch_nso<W, E, OP_NONE>(p, st, od, n, n1, lane, ss);
-    }
+    return n;
 }
 
 // ---------------------------------------------------------------------------
@@ -520,7 +640,6 @@ __global__ void __launch_bounds__(256, 2) unit_kernel(const __grid_constant__ KP
     const int lane = threadIdx.x & 31;
     Odometer<W, E> od;
     od.L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
-    od.t = st.t;
     od.gt_e = reinterpret_cast<const W *>(p.gtbl) + (size_t)(lane & (E - 1)) * p.gtbl_len;
     od.R0 = p.R0;
     od.RG = p.RG;
@@ -558,7 +677,7 @@ __global__ void __launch_bounds__(256, 2) unit_kernel(const __grid_constant__ KP
                     direct_range<W>(p, st, n, pstop, false, ss.count);
                     n = pstop;
                 } else {
-                    n = process_pblock<W, E>(p, st, od, n, pstop, lane, ss);
+                    n = run_pblock<W, E>(p, st, od, n, pstop, lane, ss);
                 }
                 if (early && n < c1 && n > read_best(p))
                     break;  // everything left in this piece ranks above a hit
@@ -1116,7 +1235,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         c->tbl_len = soff;
     }
     auto pad16 = [](uint64_t b) { return (uint32_t)((b + 15) & ~15ull); };
-    c->tbl_bytes = pad16((uint64_t)c->tbl_len * c->wbytes);
+    c->tbl_bytes = pad16((uint64_t)(c->tbl_len + 128) * c->wbytes);  // +128: unrolled reads past a row
     c->ex_bytes = pad16((uint64_t)n * (k + 1) * c->wbytes);
     c->stage_examples = c->ex_bytes <= 32 * 1024;
     c->block_threads = o.block_threads ? o.block_threads : 256;

@@ -102,6 +102,15 @@ __device__ __forceinline__ int find_split(const Tabs *t, int sz, uint64_t &r)
     return j;
 }
 
+// The decoder tables sit at offset 0 of the dynamic shared memory of every
+// scan kernel; reading them through this symbol lets the compiler emit LDS
+// (a pointer passed through a non-inlined call degrades to generic loads).
+__device__ __forceinline__ const Tabs *stabs()
+{
+    extern __shared__ __align__(16) unsigned char smem_tabs_[];
+    return reinterpret_cast<const Tabs *>(smem_tabs_);
+}
+
 __device__ __forceinline__ uint64_t globaltimer_ns()
 {
     uint64_t v;
@@ -315,6 +324,113 @@ struct SegList {
     }
 };
 
+// Chain in application order (first segment applied first); `then` appends a
+// function applied after everything already in the chain, merging it into the
+// last segment when the composition stays a single LOP3+IMAD pair.
+template <class W, int CAP>
+struct SegChain {
+    Seg<W> s[CAP];
+    int n;
+    bool a_id;  // last segment's affine part is the identity (structurally)
+    bool ovf;
+    __device__ __forceinline__ void init()
+    {
+        n = 0;
+        a_id = true;
+        ovf = false;
+#pragma unroll
+        for (int i = 0; i < CAP; ++i)
+            s[i] = seg_identity<W>();
+    }
+    __device__ __forceinline__ void push(W m, W x, W a, W b, bool aid)
+    {
+        if (n >= CAP) {
+            ovf = true;
+            return;
+        }
+#pragma unroll
+        for (int i = 0; i < CAP; ++i)
+            if (i == n)
+                s[i] = Seg<W>{m, x, a, b};
+        ++n;
+        a_id = aid;
+    }
+    __device__ __forceinline__ Seg<W> last() const
+    {
+        Seg<W> r = seg_identity<W>();
+#pragma unroll
+        for (int i = 0; i < CAP; ++i)
+            if (i == n - 1)
+                r = s[i];
+        return r;
+    }
+    __device__ __forceinline__ void set_last(const Seg<W> &v)
+    {
+#pragma unroll
+        for (int i = 0; i < CAP; ++i)
+            if (i == n - 1)
+                s[i] = v;
+    }
+    // v -> (v & m) ^ x applied after the chain
+    __device__ __forceinline__ void then_bitwise(W m, W x)
+    {
+        if (n > 0 && a_id) {
+            Seg<W> c = last();  // A is identity: ((v&M)^X)&m ^ x
+            c.x = (c.x & m) ^ x;
+            c.m = c.m & m;
+            set_last(c);
+        } else {
+            push(m, x, (W)1, (W)0, true);
+        }
+    }
+    // v -> a*v + b applied after the chain: always merges
+    __device__ __forceinline__ void then_affine(W a, W b)
+    {
+        if (n > 0) {
+            Seg<W> c = last();
+            c.b = a * c.b + b;
+            c.a = a * c.a;
+            set_last(c);
+            a_id = false;
+        } else {
+            push((W)~(W)0, (W)0, a, b, false);
+        }
+    }
+    __device__ __forceinline__ void then_seg(const Seg<W> &g)
+    {
+        then_bitwise(g.m, g.x);
+        then_affine(g.a, g.b);
+    }
+};
+
+// fixed-operand form of P: left operand fixed (v = right value)
+template <class W, int CAP>
+__device__ __forceinline__ void chain_left_fixed(SegChain<W, CAP> &c, int op, W s)
+{
+    switch (op) {
+    case OP_AND: c.then_bitwise(s, (W)0); break;
+    case OP_OR: c.then_bitwise((W)~s, s); break;
+    case OP_XOR: c.then_bitwise((W)~(W)0, s); break;
+    case OP_ADD: c.then_affine((W)1, s); break;
+    case OP_SUB: c.then_affine((W)~(W)0, s); break;  // s - v
+    default: c.then_affine(s, (W)0); break;          // MUL
+    }
+}
+
+// fixed-operand form of P: right operand fixed (v = left value)
+template <class W, int CAP>
+__device__ __forceinline__ void chain_right_fixed(SegChain<W, CAP> &c, int op, W r)
+{
+    switch (op) {
+    case OP_AND: c.then_bitwise(r, (W)0); break;
+    case OP_OR: c.then_bitwise((W)~r, r); break;
+    case OP_XOR: c.then_bitwise((W)~(W)0, r); break;
+    case OP_ADD: c.then_affine((W)1, r); break;
+    case OP_SUB: c.then_affine((W)1, (W)0 - r); break;  // v - r
+    default: c.then_affine(r, (W)0); break;            // MUL
+    }
+}
+
 template <class W, int N>
 __device__ __forceinline__ W segs_apply(const Seg<W> (&s)[N], W v)
 {
@@ -333,8 +449,9 @@ __device__ __forceinline__ W segs_apply(const Seg<W> (&s)[N], W v)
 // whose values come from the per-spec value table (tbl_e[toff[size] + rank]).  Post-order folding on
 // an explicit frame stack; control flow depends on (sz, r) only.
 template <class W>
-__device__ __noinline__ W eval_subtree(const Tabs *t, const W *tbl_e, int R0, int sz, uint64_t r)
+__device__ __noinline__ W eval_subtree(const W *tbl_e, int R0, int sz, uint64_t r)
 {
+    const Tabs *t = stabs();
     int8_t fop[MAXS], fstate[MAXS], frsz[MAXS];
     uint64_t frr[MAXS];
     W fval[MAXS];
@@ -435,7 +552,6 @@ struct WarpLevels {
 template <class W, int E>
 struct Odometer {
     WarpLevels<W, E> *L;   // this warp's shared-memory levels
-    const Tabs *t;
     const W *gt_e;         // this lane's example: values of all subtrees of size <= RG
     int R0, RG, s, lane, ex;
     // outer state
@@ -450,6 +566,7 @@ struct Odometer {
     uint64_t qb, qend;     // L1 region in q-space [qb, qend)
     Seg<W> so[MAXSO], sl[MAXSL];
     int nso, nsl;
+    bool so0_bw;           // innermost outer segment has a bitwise part
     bool ovf_o, ovf_l;
 
     __device__ __forceinline__ void reset()
@@ -462,14 +579,15 @@ struct Odometer {
 
     __device__ __forceinline__ W sib_value(int j, uint64_t q) const
     {
+        const Tabs *t = stabs();
         if (j <= RG)
             return gt_e[t->toff[j] + (uint32_t)q];
-        return eval_subtree<W>(t, gt_e, RG, j, q);
+        return eval_subtree<W>(gt_e, RG, j, q);
     }
 
     template <int CAP>
     __device__ __forceinline__ void compose(const LevelStack<W, E> &st, int nlev, Seg<W> (&out)[CAP], int &nseg,
-                                            bool &ovf) const
+                                            bool &ovf, bool &bw0) const
     {
         SegList<W, CAP> sgl;
         sgl.init();
@@ -483,6 +601,7 @@ struct Odometer {
         sgl.finalize(out);
         nseg = sgl.has ? sgl.nd + 1 : 0;
         ovf = sgl.ovf;
+        bw0 = sgl.has && sgl.cur_bw;
     }
 
     // Walk a right spine from (sz, r) at region base `rb` (same space as the
@@ -502,6 +621,7 @@ struct Odometer {
 
     __device__ __noinline__ void decode_outer(uint64_t n)
     {
+        const Tabs *t = stabs();
         LevelStack<W, E> &st = L->outer;
         if (have_outer) {
             while (no > 0 && n >= st.end[no - 1])
@@ -544,7 +664,7 @@ struct Odometer {
             pend = pb + t->T[sz];
         }
         __syncwarp();
-        compose<MAXSO>(st, no, so, nso, ovf_o);
+        compose<MAXSO>(st, no, so, nso, ovf_o, so0_bw);
         have_outer = true;
         have_x = false;
         nx = 0;
@@ -552,6 +672,7 @@ struct Odometer {
 
     __device__ __noinline__ void decode_x(uint64_t q)
     {
+        const Tabs *t = stabs();
         LevelStack<W, E> &st = L->xs;
         if (pj <= RG) {
             sz1 = pj;
@@ -589,7 +710,8 @@ struct Odometer {
             qend = qb + t->T[sz];
         }
         __syncwarp();
-        compose<MAXSL>(st, nx, sl, nsl, ovf_l);
+        bool bw_unused;
+        compose<MAXSL>(st, nx, sl, nsl, ovf_l, bw_unused);
         have_x = true;
     }
 
