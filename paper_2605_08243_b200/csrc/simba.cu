@@ -199,18 +199,37 @@ __device__ __forceinline__ void bcast_seg_array(const Seg<W> (&in)[N], int src, 
     }
 }
 
+// X-unit description: the left value of row d1 is
+//   x2d:  LEFT( pxop( G[offy + d1 / R1p], G[off1 + d1 % R1p] ) )
+//   else: LEFT( G[off1 + d1] )
+struct XU {
+    int x2d, pxop, szy, sz1;
+    uint32_t offy, off1;
+    uint64_t R1p;
+};
+
+template <class W>
+__device__ __forceinline__ W left_input(const W *g, const XU &xu, uint64_t dy, uint64_t d1p)
+{
+    if (xu.x2d)
+        return apply_bin<W>(xu.pxop, g[xu.offy + dy], g[xu.off1 + d1p]);
+    return g[xu.off1 + d1p];
+}
+
 // Rare path: at least one lane matched example 0 through the tables.  Refine
 // on examples 1..E-1 (their segments live in lanes 1..E-1 of the odometer),
 // then verify the survivors against every example with the reference-exact
 // evaluator (decode_tokens + eval_rpn).
 template <class W, int E>
-__device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
-                                     uint64_t ubase, uint32_t R2, uint32_t off1, uint32_t off2, bool hit,
-                                     uint32_t d1, uint32_t d2, uint64_t &my_count)
+__device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop, XU xu,
+                                     uint64_t ubase, uint32_t R2, uint32_t off2, bool hit, uint64_t d1, uint32_t d2,
+                                     uint64_t &my_count)
 {
     const W *gtbl = reinterpret_cast<const W *>(p.gtbl);
     const W *ys = reinterpret_cast<const W *>(st.ys);
     const W mask = (W)p.mask;
+    const uint64_t dy = xu.x2d ? d1 / xu.R1p : 0;
+    const uint64_t d1p = xu.x2d ? d1 - dy * xu.R1p : d1;
 #pragma unroll
     for (int e = 1; e < E; ++e) {
         Seg<W> so[MAXSO], sl[MAXSL];
@@ -221,13 +240,13 @@ __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const O
             const W vR = te[off2 + d2];
             W v = vR;
             if (pop != OP_NONE)
-                v = apply_bin<W>(pop, segs_apply(sl, te[off1 + d1]), vR);
+                v = apply_bin<W>(pop, segs_apply(sl, left_input(te, xu, dy, d1p)), vR);
             v = segs_apply(so, v);
             hit = (((v ^ ys[e]) & mask) == 0);
         }
     }
     if (hit) {
-        const uint64_t rank = ubase + (uint64_t)d1 * R2 + d2;
+        const uint64_t rank = ubase + d1 * R2 + d2;
         if (full_check<W>(p, st, rank))
             record_hit(p, rank, my_count);
     }
@@ -246,10 +265,9 @@ __device__ __forceinline__ W chain_apply(const Seg<W> (&c)[N], W v)
 enum : int { PJ_NONE = 0, PJ_MERGE_BW = 1, PJ_MERGE_AFF = 2, PJ_SEPARATE = 3 };
 
 template <class W>
-__device__ __forceinline__ void pseg_left_fixed(int pop, W s, Seg<W> &g, bool &bitwise)
+__device__ __forceinline__ Seg<W> first_seg(int pj, int pop, W s, const Seg<W> &so0)
 {
-    g = seg_identity<W>();
-    bitwise = (pop == OP_AND || pop == OP_OR || pop == OP_XOR);
+    Seg<W> g = seg_identity<W>();
     switch (pop) {
     case OP_AND: g.m = s; break;
     case OP_OR: g.m = ~s; g.x = s; break;
@@ -258,15 +276,6 @@ __device__ __forceinline__ void pseg_left_fixed(int pop, W s, Seg<W> &g, bool &b
     case OP_SUB: g.a = (W)~(W)0; g.b = s; break;
     default: g.a = s; break;  // MUL
     }
-}
-
-// first chain segment for a row with left value vX
-template <class W>
-__device__ __forceinline__ Seg<W> first_seg(int pj, int pop, W vX, const Seg<W> &so0)
-{
-    Seg<W> g;
-    bool bw;
-    pseg_left_fixed(pop, vX, g, bw);
     if (pj == PJ_MERGE_BW) {  // so0's bitwise part after g's
         Seg<W> r = so0;
         r.m = g.m & so0.m;
@@ -279,16 +288,16 @@ __device__ __forceinline__ Seg<W> first_seg(int pj, int pop, W vX, const Seg<W> 
         r.a = so0.a * g.a;
         return r;
     }
-    return g;  // PJ_SEPARATE (or P absent: unused)
+    return g;  // PJ_SEPARATE
 }
 
-// Variant A: R2 >= 32, lanes over d2 (4 x 32 per step), d1 uniform per row.
+// Variant A: R2 >= 32, lanes over d2 (4 x 32 per step), rows d1 uniform.
 // c[0] is rebuilt per row from the row's left value; c[1..NT-1] are fixed.
 template <class W, int E, int NT>
 __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop, int pj,
                                      const Seg<W> &so0, const Seg<W> (&rest)[NT], const Seg<W> (&sl)[MAXSL], W y0,
-                                     uint64_t ubase, uint32_t R2, uint32_t off1, uint32_t off2, uint32_t d1s,
-                                     uint32_t d2s, uint64_t u1, int lane, uint64_t &my_count)
+                                     XU xu, uint64_t ubase, uint32_t R2, uint32_t off2, uint64_t d1s, uint32_t d2s,
+                                     uint64_t u1, int lane, uint64_t &my_count)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));  // example 0, sizes <= R0 (LDS)
@@ -296,24 +305,32 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
     const W mask = (W)p.mask;
     Seg<W> c[NT];
 #pragma unroll
-    for (int i = 1; i < NT; ++i)
+    for (int i = 0; i < NT; ++i)
         c[i] = rest[i];
-    c[0] = rest[0];
     uint32_t dlo = d2s;
-    W gnext = (W)0;
+    uint64_t dy = 0, d1p = d1s;
+    if (xu.x2d) {
+        dy = d1s / xu.R1p;
+        d1p = d1s - dy * xu.R1p;
+    }
+    W lnext = (W)0;
     if (pop != OP_NONE)
-        gnext = g0[off1 + d1s];
+        lnext = left_input(g0, xu, dy, d1p);
     const W *tr = t0 + off2 + lane;
-    for (uint32_t d1 = d1s;; ++d1, dlo = 0) {
-        const uint64_t row = (uint64_t)d1 * R2;
+    for (uint64_t d1 = d1s;; ++d1, dlo = 0) {
+        const uint64_t row = d1 * R2;
         if (row >= u1)
             break;
         const uint32_t dhi = (uint32_t)min((uint64_t)R2, u1 - row);
         if (pop != OP_NONE) {
-            const W vX = segs_apply(sl, gnext);
-            if (row + R2 < u1)
-                gnext = g0[off1 + d1 + 1];  // prefetch the next row's left value
-            c[0] = first_seg(pj, pop, vX, so0);
+            c[0] = first_seg(pj, pop, segs_apply(sl, lnext), so0);
+            if (row + R2 < u1) {  // prefetch the next row's left input
+                if (++d1p == xu.R1p && xu.x2d) {
+                    d1p = 0;
+                    ++dy;
+                }
+                lnext = left_input(g0, xu, dy, d1p);
+            }
         }
         for (uint32_t it = dlo; it < dhi; it += 128) {
             // the shared table is padded by 128 words: reads past a row are harmless
@@ -327,22 +344,22 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
             const bool h2 = d2 + 64 < dhi && ((v2 ^ y0) & mask) == 0;
             const bool h3 = d2 + 96 < dhi && ((v3 ^ y0) & mask) == 0;
             if (__any_sync(FULL, h0 || h1 || h2 || h3)) {
-                on_hits<W, E>(p, st, od, pop, ubase, R2, off1, off2, h0, d1, d2, my_count);
-                on_hits<W, E>(p, st, od, pop, ubase, R2, off1, off2, h1, d1, d2 + 32, my_count);
-                on_hits<W, E>(p, st, od, pop, ubase, R2, off1, off2, h2, d1, d2 + 64, my_count);
-                on_hits<W, E>(p, st, od, pop, ubase, R2, off1, off2, h3, d1, d2 + 96, my_count);
+                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h0, d1, d2, my_count);
+                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h1, d1, d2 + 32, my_count);
+                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h2, d1, d2 + 64, my_count);
+                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h3, d1, d2 + 96, my_count);
             }
         }
     }
 }
 
 // Variant B: R2 < 32, lanes over (d1, d2) pairs (G = 32 / R2 rows per step,
-// 4 steps per iteration); the lane's chain LEFT, P(., vR), OUTER is fixed.
+// 4 steps per iteration); the lane's chain LEFT, P(., vR), OUTER is fixed and
+// its input is the row's left input (one or two table reads).
 template <class W, int E, int NT>
 __device__ __noinline__ void sweep_b(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
-                                     const Seg<W> (&c)[NT], W y0, uint64_t ubase, uint32_t R2, uint32_t off1,
-                                     uint32_t off2, uint32_t d1s, uint64_t u0, uint64_t u1, int lane,
-                                     uint64_t &my_count)
+                                     const Seg<W> (&c)[NT], W y0, XU xu, uint64_t ubase, uint32_t R2, uint32_t off2,
+                                     uint64_t d1s, uint64_t u0, uint64_t u1, int lane, uint64_t &my_count)
 {
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);
     const W mask = (W)p.mask;
@@ -350,24 +367,46 @@ __device__ __noinline__ void sweep_b(const KParams &p, const Staged &st, const O
     const uint32_t lg = (uint32_t)lane / R2;
     const uint32_t ld2 = (uint32_t)lane - lg * R2;
     const bool lane_ok = lg < G;
-    const W *rowp = g0 + off1;
-    const uint32_t d1e = (uint32_t)((u1 + R2 - 1) / R2);  // first row past the unit range
-    for (uint32_t d1b = d1s; d1b < d1e; d1b += 4 * G) {
+    const uint64_t d1e = (u1 + R2 - 1) / R2;  // first row past the unit range
+    // per-lane row cursor (dy, d1p) for row d1s + lg, stepped by G
+    uint64_t dy = 0, d1p = d1s + lg;
+    uint64_t qG = 0, rG = G;
+    if (xu.x2d) {
+        dy = d1p / xu.R1p;
+        d1p -= dy * xu.R1p;
+        qG = G / xu.R1p;
+        rG = G - qG * xu.R1p;
+    }
+    for (uint64_t d1b = d1s; d1b < d1e; d1b += 4 * G) {
         bool h[4];
-        uint32_t d1v[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t d1 = d1b + k * G + lg;
-            const uint64_t uu = (uint64_t)d1 * R2 + ld2;
+            const uint64_t d1 = d1b + k * G + lg;
+            const uint64_t uu = d1 * R2 + ld2;
             const bool act = lane_ok && uu >= u0 && uu < u1;
-            const W v = chain_apply(c, rowp[act ? d1 : d1s]);
+            W in = (W)0;
+            if (pop == OP_NONE)
+                in = (W)0;
+            else if (act)
+                in = left_input(g0, xu, dy, d1p);
+            const W v = chain_apply(c, in);
             h[k] = act && ((v ^ y0) & mask) == 0;
-            d1v[k] = d1;
+            if (xu.x2d) {
+                d1p += rG;
+                dy += qG;
+                if (d1p >= xu.R1p) {
+                    d1p -= xu.R1p;
+                    ++dy;
+                }
+            } else {
+                d1p += G;
+            }
         }
         if (__any_sync(FULL, h[0] || h[1] || h[2] || h[3])) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                on_hits<W, E>(p, st, od, pop, ubase, R2, off1, off2, h[k], h[k] ? d1v[k] : 0, ld2, my_count);
+                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h[k], h[k] ? d1b + k * G + lg : 0, ld2,
+                              my_count);
         }
     }
 }
@@ -387,28 +426,28 @@ struct SweepStats {
 template <class W, int E, int NT>
 __device__ __forceinline__ void dispatch_a_nt(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
                                               int pj, const Seg<W> &so0, const Seg<W> (&chain)[8],
-                                              const Seg<W> (&sl)[MAXSL], W y0, uint64_t ubase, uint32_t R2,
-                                              uint32_t off1, uint32_t off2, uint32_t d1s, uint32_t d2s, uint64_t u1,
+                                              const Seg<W> (&sl)[MAXSL], W y0, const XU &xu, uint64_t ubase,
+                                              uint32_t R2, uint32_t off2, uint64_t d1s, uint32_t d2s, uint64_t u1,
                                               int lane, uint64_t &cnt)
 {
     Seg<W> rest[NT];
 #pragma unroll
     for (int i = 0; i < NT; ++i)
         rest[i] = chain[i];
-    sweep_a<W, E, NT>(p, st, od, pop, pj, so0, rest, sl, y0, ubase, R2, off1, off2, d1s, d2s, u1, lane, cnt);
+    sweep_a<W, E, NT>(p, st, od, pop, pj, so0, rest, sl, y0, xu, ubase, R2, off2, d1s, d2s, u1, lane, cnt);
 }
 
 template <class W, int E, int NT>
 __device__ __forceinline__ void dispatch_b_nt(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
-                                              const Seg<W> (&chain)[8], W y0, uint64_t ubase, uint32_t R2,
-                                              uint32_t off1, uint32_t off2, uint32_t d1s, uint64_t u0, uint64_t u1,
+                                              const Seg<W> (&chain)[8], W y0, const XU &xu, uint64_t ubase,
+                                              uint32_t R2, uint32_t off2, uint64_t d1s, uint64_t u0, uint64_t u1,
                                               int lane, uint64_t &cnt)
 {
     Seg<W> c[NT];
 #pragma unroll
     for (int i = 0; i < NT; ++i)
         c[i] = chain[i];
-    sweep_b<W, E, NT>(p, st, od, pop, c, y0, ubase, R2, off1, off2, d1s, u0, u1, lane, cnt);
+    sweep_b<W, E, NT>(p, st, od, pop, c, y0, xu, ubase, R2, off2, d1s, u0, u1, lane, cnt);
 }
 
 // All ranks [n, n1) of one P block (n1 <= pend).  The outer chain and P's
@@ -465,8 +504,9 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
         }
     }
     while (n < n1) {
-        uint64_t ubase, R1 = 1, stop;
-        uint32_t off1 = 0, d1s = 0, d2s;
+        uint64_t ubase, stop, d1s = 0;
+        uint32_t d2s;
+        XU xu{0, 0, 0, 0, 0, 0, 1};
         if (pop == OP_NONE) {
             ubase = pb;
             d2s = (uint32_t)(n - pb);
@@ -479,11 +519,18 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
             d2s = (uint32_t)(rel - q * R2);
             if (!od.have_x || q >= od.qend)
                 od.decode_x(q);
-            R1 = t->T[od.sz1];
-            off1 = t->toff[od.sz1];
+            xu.x2d = od.x2d ? 1 : 0;
+            xu.sz1 = od.sz1;
+            xu.off1 = t->toff[od.sz1];
+            xu.R1p = t->T[od.sz1];
+            if (od.x2d) {
+                xu.pxop = od.pxop;
+                xu.szy = od.szy;
+                xu.offy = t->toff[od.szy];
+            }
             ubase = pb + od.qb * R2;
-            d1s = (uint32_t)(q - od.qb);
-            stop = min(ubase + R1 * R2, n1);
+            d1s = q - od.qb;
+            stop = min(pb + od.qend * R2, n1);
         }
         ++ss.units;
         if (od.ovf_l) {
@@ -502,16 +549,16 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
             const uint64_t u0 = n - ubase, u1 = stop - ubase;
             if (R2 >= 32) {
                 if (ntA <= 1)
-                    dispatch_a_nt<W, E, 1>(p, st, od, pop, pj, so[0], chainA, sl, y0, ubase, R2, off1, off2, d1s,
+                    dispatch_a_nt<W, E, 1>(p, st, od, pop, pj, so[0], chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
                 else if (ntA == 2)
-                    dispatch_a_nt<W, E, 2>(p, st, od, pop, pj, so[0], chainA, sl, y0, ubase, R2, off1, off2, d1s,
+                    dispatch_a_nt<W, E, 2>(p, st, od, pop, pj, so[0], chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
                 else if (ntA == 3)
-                    dispatch_a_nt<W, E, 3>(p, st, od, pop, pj, so[0], chainA, sl, y0, ubase, R2, off1, off2, d1s,
+                    dispatch_a_nt<W, E, 3>(p, st, od, pop, pj, so[0], chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
                 else
-                    dispatch_a_nt<W, E, 5>(p, st, od, pop, pj, so[0], chainA, sl, y0, ubase, R2, off1, off2, d1s,
+                    dispatch_a_nt<W, E, 5>(p, st, od, pop, pj, so[0], chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
             } else {
                 // lane chain: LEFT, P(., vR), OUTER with vR = this lane's d2 value
@@ -525,20 +572,19 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
                         ch.then_seg(sl[i]);
                     chain_right_fixed(ch, pop, vR);
                 } else {
-                    ch.then_affine((W)0, vR);  // value = vR whatever the row value
+                    ch.then_affine((W)0, vR);  // value = vR whatever the row input
                 }
                 for (int i = 0; i < nso; ++i)
                     ch.then_seg(so[i]);
-                int nt = ch.n;
-                nt = __reduce_max_sync(FULL, (unsigned)nt);
+                const int nt = (int)__reduce_max_sync(FULL, (unsigned)ch.n);
                 if (nt <= 2)
-                    dispatch_b_nt<W, E, 2>(p, st, od, pop, ch.s, y0, ubase, R2, off1, off2, d1s, u0, u1, lane,
+                    dispatch_b_nt<W, E, 2>(p, st, od, pop, ch.s, y0, xu, ubase, R2, off2, d1s, u0, u1, lane,
                                            ss.count);
                 else if (nt <= 4)
-                    dispatch_b_nt<W, E, 4>(p, st, od, pop, ch.s, y0, ubase, R2, off1, off2, d1s, u0, u1, lane,
+                    dispatch_b_nt<W, E, 4>(p, st, od, pop, ch.s, y0, xu, ubase, R2, off2, d1s, u0, u1, lane,
                                            ss.count);
                 else
-                    dispatch_b_nt<W, E, 8>(p, st, od, pop, ch.s, y0, ubase, R2, off1, off2, d1s, u0, u1, lane,
+                    dispatch_b_nt<W, E, 8>(p, st, od, pop, ch.s, y0, xu, ubase, R2, off2, d1s, u0, u1, lane,
                                            ss.count);
             }
         }
@@ -1210,7 +1256,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         const uint64_t cap = std::max<uint64_t>(tbl_size(R0), tbl_size(max_size) / 16);
         RG = R0;
         for (int r = R0 + 1; r <= max_size - 2; ++r) {
-            if (t.T[r] >= (1ull << 27) || tbl_size(r) > (16ull << 20) || tbl_size(r) > cap)
+            if (t.T[r] >= (1ull << 27) || tbl_size(r) > (24ull << 20) || tbl_size(r) > cap)
                 break;
             RG = r;
         }

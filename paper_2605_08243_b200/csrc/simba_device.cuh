@@ -562,8 +562,10 @@ struct Odometer {
     // X state
     int nx;
     bool have_x;
-    int sz1;
-    uint64_t qb, qend;     // L1 region in q-space [qb, qend)
+    int sz1;               // size of L1 (the last digit of X)
+    bool x2d;              // X's last node N_X has both children <= RG: digits (dy, d1')
+    int pxop, szy;         // N_X's operator and left-child size (x2d)
+    uint64_t qb, qend;     // X-unit region in q-space [qb, qend)
     Seg<W> so[MAXSO], sl[MAXSL];
     int nso, nsl;
     bool so0_bw;           // innermost outer segment has a bitwise part
@@ -676,6 +678,7 @@ struct Odometer {
         LevelStack<W, E> &st = L->xs;
         if (pj <= RG) {
             sz1 = pj;
+            x2d = false;
             qb = 0;
             qend = t->T[pj];
             nx = 0;
@@ -689,6 +692,7 @@ struct Odometer {
             int sz = (nx == 0) ? pj : st.csz[nx - 1];
             const uint64_t rb = (nx == 0) ? 0 : st.end[nx - 1] - t->T[sz];
             uint64_t r = q - rb;
+            x2d = false;
             while (sz > RG) {
                 const int op = find_slot(t, sz, r);
                 if (op == OP_NOT || op == OP_NEG) {
@@ -698,6 +702,17 @@ struct Odometer {
                 }
                 const int j = find_split(t, sz, r);
                 const int rsz = sz - 1 - j;
+                if (rsz <= RG && j <= RG) {
+                    // N_X: both children are table digits; the X-unit is the
+                    // whole (op, j) split block of this node (left-major)
+                    x2d = true;
+                    pxop = op;
+                    szy = j;
+                    sz1 = rsz;
+                    qb = q - r;
+                    qend = qb + t->T[j] * t->T[rsz];
+                    break;
+                }
                 const uint64_t qq = div_T(t, rsz, r);
                 const uint64_t rr = r - qq * t->T[rsz];
                 const W sv = sib_value(j, qq);
@@ -705,9 +720,11 @@ struct Odometer {
                 sz = rsz;
                 r = rr;
             }
-            sz1 = sz;
-            qb = q - r;
-            qend = qb + t->T[sz];
+            if (!x2d) {
+                sz1 = sz;
+                qb = q - r;
+                qend = qb + t->T[sz];
+            }
         }
         __syncwarp();
         bool bw_unused;

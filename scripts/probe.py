@@ -13,22 +13,27 @@ def unsat(k, w, n, seed):
     return S.Specification(k=k, w=w, pairs=tuple(pairs))
 
 def run(label, spec, sizes, **kw):
+    t0 = time.perf_counter()
     with DeviceContext(spec, max(sizes), **kw) as ctx:
         info = ctx.info()
+        tc = time.perf_counter() - t0
         for s in sizes:
             r = ctx.count(s)  # warm
             r = ctx.count(s)
-            print(f"{label:28s} s={s:2d} T={r.visited:.3e} kernel={r.kernel_ms:9.3f} ms  "
-                  f"{r.visited / (r.kernel_ms * 1e-3):.3e} cand/s  count={r.count} units={r.units} rank_units={r.rank_units} {info}", flush=True)
+            print(f"{label:22s} s={s:2d} T={r.visited:.3e} {r.kernel_ms:9.3f} ms "
+                  f"{r.visited / (r.kernel_ms * 1e-3):.3e} cand/s cnt={r.count} units={r.units} "
+                  f"rank_units={r.rank_units} ctx={tc*1e3:.0f}ms {info}", flush=True)
 
 spec4 = unsat(4, 32, 10, 31337)
 if len(sys.argv) > 1:
-    run("C5 unit", spec4, [int(sys.argv[1])]); sys.exit()
-run("C5 unit", spec4, [9, 10, 11, 12])
+    run("C5 unit", spec4, [int(a) for a in sys.argv[1:]]); sys.exit()
+run("C5 unit", spec4, [9, 10, 11, 12, 13])
+run("C5 unit rg=8", spec4, [12, 13], rg=8)
 run("C5 direct", spec4, [9, 10], kernel="direct")
 run("C5 unit r0=4", spec4, [11], r0=4)
-run("C5 unit r0=3", spec4, [11], r0=3)
 spec3 = unsat(3, 32, 10, 777)
-run("C3 unit", spec3, [9, 10, 11])
+run("C3 unit", spec3, [9, 10, 11, 12])
 spec4w = unsat(3, 64, 100, 4242)
-run("C4 unit", spec4w, [9, 10])
+run("C4 unit", spec4w, [9, 10, 11])
+spec2 = unsat(2, 32, 10, 99)
+run("C2 unit", spec2, [7, 10, 13])
