@@ -96,6 +96,7 @@ typedef struct {
     uint64_t launches;   /* kernels launched for this call */
     uint64_t units;      /* units decoded by the unit kernel */
     uint64_t rank_units; /* units that took the per-rank path */
+    uint64_t ex0_hits;   /* candidates matching example 0 (for the e-bar statistic) */
 } simba_result;
 
 /* engine._scan_range(ctx, size, offset, block_total, start, stop, shuffled)
@@ -155,6 +156,17 @@ int simba_decode(simba_ctx *ctx, uint64_t rank, int size, int32_t *tokens);
  * examples, word bytes, grid blocks, block threads, shared-memory bytes per block. */
 int simba_ctx_info(simba_ctx *ctx, int *r0, int *rg, int *table_examples, int *word_bytes, int *grid_blocks,
                    int *block_threads, int *smem_bytes);
+
+/* Host->device and device->host bytes this context has copied so far. */
+int simba_ctx_bytes(simba_ctx *ctx, uint64_t *h2d, uint64_t *d2h);
+
+/* The CUDA stream (cudaStream_t) the context launches on, for callers that
+ * record their own events around calls. */
+int simba_ctx_stream(simba_ctx *ctx, void **stream);
+
+/* INT32 issue-rate probe (roofline denominator): independent LOP3->IMAD
+ * chains on every SM; reports integer ops/s and the kernel time. */
+int simba_int32_peak(int device, int iters, double *ops_per_s, double *kernel_ms);
 
 const char *simba_last_error(void);
 int simba_device_count(void);

@@ -47,6 +47,7 @@ class Result(C.Structure):
         ("launches", C.c_uint64),
         ("units", C.c_uint64),
         ("rank_units", C.c_uint64),
+        ("ex0_hits", C.c_uint64),
     ]
 
 
@@ -92,6 +93,9 @@ SIGNATURES = {
     "simba_synthesize": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_double, C.POINTER(Outcome)]),
     "simba_decode": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
     "simba_ctx_info": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int)] * 7),
+    "simba_ctx_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "simba_ctx_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "simba_int32_peak": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "simba_last_error": (C.c_char_p, []),
     "simba_device_count": (C.c_int, []),
     "simba_launch_count": (C.c_uint64, []),
@@ -101,7 +105,7 @@ SIGNATURES = {
 def _load():
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH} is not built; run `python __graft_entry__.py` (nvcc, sm_100a). "
+            f"{LIB_PATH} is not built; run `python __graft_entry__.py` or `python paper_2605_08243_b200/_build.py` (nvcc, sm_100a). "
             "The SIMBA device path has no CPU fallback.")
     lib = C.CDLL(str(LIB_PATH))
     for name, (res, args) in SIGNATURES.items():

@@ -149,6 +149,11 @@ __device__ __noinline__ void direct_range(const KParams &p, const Staged &st, ui
             decode_tokens(st.t, rank, p.s, buf);
             alive = (((eval_rpn<W, W>(buf, p.s, xs) ^ ys[0]) & mask) == 0);
         }
+        {
+            const unsigned hits0 = __popc(__ballot_sync(FULL, alive));
+            if ((threadIdx.x & 31) == 0 && hits0)
+                atomicAdd(&p.units[3], (unsigned long long)hits0);  // example-0 matches (for e-bar)
+        }
         for (int e = 1; e < p.n; ++e) {
             if (!__any_sync(FULL, alive))
                 break;
@@ -228,6 +233,9 @@ __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const O
     const W *gtbl = reinterpret_cast<const W *>(p.gtbl);
     const W *ys = reinterpret_cast<const W *>(st.ys);
     const W mask = (W)p.mask;
+    const unsigned hits0 = __popc(__ballot_sync(FULL, hit));
+    if ((threadIdx.x & 31) == 0 && hits0)
+        atomicAdd(&p.units[3], (unsigned long long)hits0);  // example-0 matches (for e-bar)
     const uint64_t dy = xu.x2d ? d1 / xu.R1p : 0;
     const uint64_t d1p = xu.x2d ? d1 - dy * xu.R1p : d1;
 #pragma unroll
@@ -782,6 +790,34 @@ __global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int RG, 
     out[idx] = eval_rpn<W, W>(buf, sz, X + (size_t)e * k);
 }
 
+// INT32 issue roofline probe: 8 independent LOP3 -> IMAD chains per thread
+// (the operator mix of the sweep loops: one ALU-pipe and one FMA-pipe op per
+// step), so ops/s = threads * iters * 16 / time.
+__global__ void __launch_bounds__(256) int32_peak_kernel(uint32_t seed, int iters, uint32_t *out)
+{
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t a[8], b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        a[u] = seed * (tid + 1) + u;
+        b[u] = seed ^ (tid * 2654435761u + u);
+    }
+    const uint32_t c = seed * 3u + 1u, d = seed * 5u + 7u;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a[u] = (a[u] & b[u]) ^ c;
+            b[u] = b[u] * a[u] + d;
+        }
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        r ^= a[u] + b[u];
+    if (r == 0x12345678u)
+        out[0] = r;
+}
+
 __global__ void decode_kernel(const Tabs *tabs, uint64_t rank, int size, int32_t *out)
 {
     int8_t buf[MAXS];
@@ -876,6 +912,7 @@ struct simba_ctx {
     unsigned long long *d_ctr = nullptr;
     unsigned long long *h_ctr = nullptr;
     int32_t *d_tok = nullptr;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this context
 };
 
 namespace {
@@ -954,6 +991,7 @@ int decode_rank(simba_ctx *c, uint64_t rank, int size, int32_t *tokens)
     g_launches++;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(tokens, c->d_tok, sizeof(int32_t) * size, cudaMemcpyDeviceToHost, c->stream));
+    c->d2h_bytes += sizeof(int32_t) * size;
     CK(cudaStreamSynchronize(c->stream));
     return SIMBA_OK;
 }
@@ -1047,6 +1085,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     BlobInfo bi{c->d_blob, c->tbl_bytes, c->ex_bytes};
     const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(c->d_ctr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    c->h2d_bytes += sizeof(init);
     CK(cudaEventRecord(c->ev0, c->stream));
     if (c->wbytes == 4)
         launch_scan<uint32_t>(c, p, bi, direct);
@@ -1056,6 +1095,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     CK(cudaEventRecord(c->ev1, c->stream));
     CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(unsigned long long) * kCtrWords, cudaMemcpyDeviceToHost,
                        c->stream));
+    c->d2h_bytes += sizeof(unsigned long long) * kCtrWords;
     CK(cudaStreamSynchronize(c->stream));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
@@ -1064,6 +1104,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     out->visited = c->h_ctr[3];
     out->units = c->h_ctr[4];
     out->rank_units = c->h_ctr[5];
+    out->ex0_hits = c->h_ctr[7];
     out->count = c->h_ctr[2];
     out->best_rank = c->h_ctr[1];
     out->completed = (c->h_ctr[6] & 1u) ? 0 : 1;
@@ -1350,6 +1391,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     }
     if ((e = cudaMemcpyAsync(c->d_tabs, &t, sizeof(Tabs), cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
         return cuda_bail(e, "upload tables");
+    c->h2d_bytes += sizeof(Tabs) + c->ex_bytes;
     if ((e = cudaMemcpyAsync(c->d_blob + c->tbl_bytes, ex.data(), c->ex_bytes, cudaMemcpyHostToDevice,
                              c->stream)) != cudaSuccess)
         return cuda_bail(e, "upload examples");
@@ -1567,6 +1609,51 @@ int simba_synthesize(simba_ctx *c, int size_bound, int shuffled, double time_bud
         }
     }
     out->status = SIMBA_STATUS_NOT_FOUND;
+    return SIMBA_OK;
+}
+
+int simba_ctx_bytes(simba_ctx *c, uint64_t *h2d, uint64_t *d2h)
+{
+    if (!c)
+        return fail(SIMBA_EINVAL, "null context");
+    *h2d = c->h2d_bytes;
+    *d2h = c->d2h_bytes;
+    return SIMBA_OK;
+}
+
+int simba_ctx_stream(simba_ctx *c, void **stream)
+{
+    if (!c || !stream)
+        return fail(SIMBA_EINVAL, "null argument");
+    *stream = (void *)c->stream;
+    return SIMBA_OK;
+}
+
+int simba_int32_peak(int device, int iters, double *ops_per_s, double *kernel_ms)
+{
+    CK(cudaSetDevice(device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    uint32_t *d_out = nullptr;
+    CK(cudaMalloc(&d_out, sizeof(uint32_t)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = sms * 8, threads = 256;
+    int32_peak_kernel<<<blocks, threads>>>(12345u, 64, d_out);  // warm-up
+    g_launches++;
+    CK(cudaEventRecord(e0));
+    int32_peak_kernel<<<blocks, threads>>>(777u, iters, d_out);
+    g_launches++;
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d_out);
+    *kernel_ms = ms;
+    *ops_per_s = (double)blocks * threads * (double)iters * 16.0 / (ms * 1e-3);
     return SIMBA_OK;
 }
 

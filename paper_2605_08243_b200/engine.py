@@ -134,6 +134,7 @@ class RangeResult:
     launches: int
     units: int = 0
     rank_units: int = 0
+    ex0_hits: int = 0
 
 
 @dataclass(frozen=True)
@@ -202,7 +203,7 @@ class DeviceContext:
             best_rank=r.best_rank if found else None,
             tokens=tuple(r.tokens[:size]) if found else None,
             completed=bool(r.completed), kernel_ms=r.kernel_ms, launches=r.launches,
-            units=r.units, rank_units=r.rank_units)
+            units=r.units, rank_units=r.rank_units, ex0_hits=r.ex0_hits)
 
     def scan_range(self, size, offset, block_total, start, stop, shuffled=False):
         """engine._scan_range (engine.py:128-156) -> (visited, best_rank, best_tokens)."""
@@ -233,6 +234,18 @@ class DeviceContext:
                                           -1.0 if time_budget is None else float(time_budget),
                                           C.byref(out)))
         return out
+
+    def copied_bytes(self) -> tuple[int, int]:
+        """(host->device, device->host) bytes this context has copied."""
+        h, d = C.c_uint64(), C.c_uint64()
+        N.check_rc(N.lib.simba_ctx_bytes(self._ptr, C.byref(h), C.byref(d)))
+        return h.value, d.value
+
+    def stream_handle(self) -> int:
+        """cudaStream_t of this context (wrap with torch.cuda.ExternalStream)."""
+        h = C.c_void_p()
+        N.check_rc(N.lib.simba_ctx_stream(self._ptr, C.byref(h)))
+        return h.value or 0
 
     def decode(self, rank: int, size: int) -> tuple[int, ...]:
         buf = (C.c_int32 * N.MAX_SIZE)()

@@ -1,0 +1,84 @@
+"""Multi-GPU sharding of the search: one process per GPU.
+
+Each size level's rank space [0, T[s][8]) is cut into super-chunks dealt
+round-robin to the ranks (super-chunk c -> rank c mod world), so every GPU
+advances through the level in ascending rank order together.  The only
+exchange is one MIN (first satisfying rank) and one SUM (count, visited) per
+size level -- 24 bytes, done with ``torch.distributed.all_reduce`` (NCCL on
+GPUs, gloo in the CPU tests).  The result equals the single-device one:
+
+* count mode: every rank is visited by exactly one shard, so the SUM is the
+  exhaustive count and the MIN the first satisfying rank;
+* search mode: a shard skips only ranks above its own best hit, so its result
+  is the exact minimum of its shard and the MIN over shards is the level's
+  minimum -- the (size, rank) the reference returns (engine.py:244-262).
+
+The device work is a ``scan(size, lo, hi, mode, shard, nshards, chunk)``
+callable (``DeviceContext.run`` on a GPU); the tests plug in the CPU oracle
+with the same chunk ownership to check the protocol on CPU with gloo.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+NO_RANK = (1 << 64) - 1
+_I64_MAX = (1 << 63) - 1
+
+
+@dataclass(frozen=True)
+class LevelResult:
+    size: int
+    count: int
+    first_rank: int | None
+    visited: int
+
+
+def _reduce(count: int, first: int | None, visited: int, device=None, group=None):
+    import torch
+    import torch.distributed as dist
+
+    if first is not None and first > _I64_MAX:
+        raise OverflowError("rank beyond int64 in the distributed reduction")
+    sums = torch.tensor([count, visited], dtype=torch.int64, device=device)
+    mins = torch.tensor([_I64_MAX if first is None else first], dtype=torch.int64, device=device)
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(mins, op=dist.ReduceOp.MIN, group=group)
+    f = int(mins.item())
+    return int(sums[0].item()), (None if f == _I64_MAX else f), int(sums[1].item())
+
+
+def run_level(scan, size: int, total: int, mode: str, rank: int, world: int, chunk: int = 0,
+              device=None, group=None) -> LevelResult:
+    """Scan size level `size` across `world` ranks and reduce.  `scan` returns
+    an object with .count, .best_rank (None if no hit) and .visited."""
+    r = scan(size, 0, total, mode, rank, world, chunk)
+    if world == 1:
+        return LevelResult(size, r.count, r.best_rank, r.visited)
+    count, first, visited = _reduce(r.count, r.best_rank, r.visited, device=device, group=group)
+    return LevelResult(size, count, first, visited)
+
+
+def count_levels(scan, totals, rank: int, world: int, chunk: int = 0, device=None, group=None):
+    """Exhaustive count of sizes 1..len(totals) (totals[s-1] = T[s][8])."""
+    return [run_level(scan, s, t, "count", rank, world, chunk, device, group)
+            for s, t in enumerate(totals, start=1)]
+
+
+def search(scan, totals, rank: int, world: int, chunk: int = 0, device=None, group=None):
+    """Algorithm 1 across ranks: sizes ascending, stop at the first size with a
+    hit.  Returns (found_size | None, rank | None, per-level results)."""
+    levels = []
+    for s, t in enumerate(totals, start=1):
+        lv = run_level(scan, s, t, "search", rank, world, chunk, device, group)
+        levels.append(lv)
+        if lv.first_rank is not None:
+            return s, lv.first_rank, levels
+    return None, None, levels
+
+
+def device_scan(ctx):
+    """Adapter: DeviceContext.run as a `scan` callable."""
+    def scan(size, lo, hi, mode, shard, nshards, chunk):
+        return ctx.run(size, lo, hi, mode=mode, chunk=chunk, shard=shard, nshards=nshards)
+    return scan
