@@ -311,10 +311,14 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
     const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));  // example 0, sizes <= R0 (LDS)
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);               // example 0, sizes <= RG (global)
     const W mask = (W)p.mask;
-    Seg<W> c[NT];
+    Seg<W> c[NT], slr[MAXSL];
 #pragma unroll
     for (int i = 0; i < NT; ++i)
         c[i] = rest[i];
+#pragma unroll
+    for (int i = 0; i < MAXSL; ++i)
+        slr[i] = sl[i];
+    const Seg<W> s0 = so0;
     uint32_t dlo = d2s;
     uint64_t dy = 0, d1p = d1s;
     if (xu.x2d) {
@@ -331,7 +335,7 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
             break;
         const uint32_t dhi = (uint32_t)min((uint64_t)R2, u1 - row);
         if (pop != OP_NONE) {
-            c[0] = first_seg(pj, pop, segs_apply(sl, lnext), so0);
+            c[0] = first_seg(pj, pop, segs_apply(slr, lnext), s0);
             if (row + R2 < u1) {  // prefetch the next row's left input
                 if (++d1p == xu.R1p && xu.x2d) {
                     d1p = 0;
@@ -352,68 +356,80 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
             const bool h2 = d2 + 64 < dhi && ((v2 ^ y0) & mask) == 0;
             const bool h3 = d2 + 96 < dhi && ((v3 ^ y0) & mask) == 0;
             if (__any_sync(FULL, h0 || h1 || h2 || h3)) {
-                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h0, d1, d2, my_count);
-                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h1, d1, d2 + 32, my_count);
-                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h2, d1, d2 + 64, my_count);
-                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h3, d1, d2 + 96, my_count);
+                const bool hk[4] = {h0, h1, h2, h3};
+                for (int k = 0; k < 4; ++k)
+                    on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, hk[k], d1, d2 + 32 * k, my_count);
             }
         }
     }
 }
 
-// Variant B: R2 < 32, lanes over (d1, d2) pairs (G = 32 / R2 rows per step,
+// Variant B: R2 < 32, lanes over (row, d2) pairs (G = 32 / R2 rows per step,
 // 4 steps per iteration); the lane's chain LEFT, P(., vR), OUTER is fixed and
-// its input is the row's left input (one or two table reads).
-template <class W, int E, int NT>
+// its input is the row's left input (one table read, or two combined by N_X's
+// operator for a two-digit X).  All per-candidate index math is 32-bit and
+// relative to the unit's first row; the chain lives in registers.
+template <class W, int E, int NT, bool X2D>
 __device__ __noinline__ void sweep_b(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
-                                     const Seg<W> (&c)[NT], W y0, XU xu, uint64_t ubase, uint32_t R2, uint32_t off2,
+                                     const Seg<W> (&cin)[NT], W y0, XU xu, uint64_t ubase, uint32_t R2, uint32_t off2,
                                      uint64_t d1s, uint64_t u0, uint64_t u1, int lane, uint64_t &my_count)
 {
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);
     const W mask = (W)p.mask;
+    Seg<W> c[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+        c[i] = cin[i];
     const uint32_t G = 32u / R2;
     const uint32_t lg = (uint32_t)lane / R2;
     const uint32_t ld2 = (uint32_t)lane - lg * R2;
     const bool lane_ok = lg < G;
-    const uint64_t d1e = (u1 + R2 - 1) / R2;  // first row past the unit range
-    // per-lane row cursor (dy, d1p) for row d1s + lg, stepped by G
-    uint64_t dy = 0, d1p = d1s + lg;
-    uint64_t qG = 0, rG = G;
-    if (xu.x2d) {
-        dy = d1p / xu.R1p;
-        d1p -= dy * xu.R1p;
-        qG = G / xu.R1p;
-        rG = G - qG * xu.R1p;
+    const uint64_t b0 = d1s * R2;                                   // unit index of row d1s, d2 = 0
+    const uint32_t nrows = (uint32_t)((u1 - b0 + R2 - 1) / R2);     // rows touched
+    const uint32_t d2first = (uint32_t)(u0 - b0);                   // first row starts here
+    const uint32_t d2last = (uint32_t)(u1 - b0 - (uint64_t)(nrows - 1) * R2);  // last row ends before
+    const bool pnone = (pop == OP_NONE);
+    // row cursor: !X2D: row value gl[rr];  X2D: (dy, d1p) of row d1s + rr
+    const W *gl = g0 + xu.off1 + d1s;
+    const W *gy = g0 + xu.offy;
+    const W *g1 = g0 + xu.off1;
+    uint32_t dy = 0, d1p = 0, qG = 0, rG = 0;
+    const uint32_t R1p = (uint32_t)xu.R1p;
+    if constexpr (X2D) {
+        const uint64_t r0 = d1s + lg;
+        dy = (uint32_t)(r0 / R1p);
+        d1p = (uint32_t)(r0 - (uint64_t)dy * R1p);
+        qG = G / R1p;
+        rG = G - qG * R1p;
     }
-    for (uint64_t d1b = d1s; d1b < d1e; d1b += 4 * G) {
-        bool h[4];
+    for (uint32_t rb = 0; rb < nrows; rb += 4 * G) {
+        bool h[4], act[4];
+        W in[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint64_t d1 = d1b + k * G + lg;
-            const uint64_t uu = d1 * R2 + ld2;
-            const bool act = lane_ok && uu >= u0 && uu < u1;
-            W in = (W)0;
-            if (pop == OP_NONE)
-                in = (W)0;
-            else if (act)
-                in = left_input(g0, xu, dy, d1p);
-            const W v = chain_apply(c, in);
-            h[k] = act && ((v ^ y0) & mask) == 0;
-            if (xu.x2d) {
+            const uint32_t rr = rb + k * G + lg;
+            act[k] = lane_ok && rr < nrows && (rr != 0 || ld2 >= d2first) && (rr + 1 != nrows || ld2 < d2last);
+            if constexpr (X2D) {
+                const W a = gy[act[k] ? dy : 0], bb = g1[act[k] ? d1p : 0];
+                in[k] = apply_bin<W>(xu.pxop, a, bb);
                 d1p += rG;
                 dy += qG;
-                if (d1p >= xu.R1p) {
-                    d1p -= xu.R1p;
+                if (d1p >= R1p) {
+                    d1p -= R1p;
                     ++dy;
                 }
             } else {
-                d1p += G;
+                in[k] = pnone ? (W)0 : gl[act[k] ? rr : 0];
             }
         }
-        if (__any_sync(FULL, h[0] || h[1] || h[2] || h[3])) {
 #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const W v = chain_apply(c, in[k]);
+            h[k] = act[k] && ((v ^ y0) & mask) == 0;
+        }
+        if (__any_sync(FULL, h[0] || h[1] || h[2] || h[3])) {
             for (int k = 0; k < 4; ++k)
-                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h[k], h[k] ? d1b + k * G + lg : 0, ld2,
+                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h[k], h[k] ? d1s + rb + k * G + lg : 0, ld2,
                               my_count);
         }
     }
@@ -455,7 +471,10 @@ __device__ __forceinline__ void dispatch_b_nt(const KParams &p, const Staged &st
 #pragma unroll
     for (int i = 0; i < NT; ++i)
         c[i] = chain[i];
-    sweep_b<W, E, NT>(p, st, od, pop, c, y0, xu, ubase, R2, off2, d1s, u0, u1, lane, cnt);
+    if (xu.x2d)
+        sweep_b<W, E, NT, true>(p, st, od, pop, c, y0, xu, ubase, R2, off2, d1s, u0, u1, lane, cnt);
+    else
+        sweep_b<W, E, NT, false>(p, st, od, pop, c, y0, xu, ubase, R2, off2, d1s, u0, u1, lane, cnt);
 }
 
 // All ranks [n, n1) of one P block (n1 <= pend).  The outer chain and P's
