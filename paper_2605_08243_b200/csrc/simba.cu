@@ -269,43 +269,48 @@ __device__ __forceinline__ W chain_apply(const Seg<W> (&c)[N], W v)
     return v;
 }
 
-// How P(vX, .) joins the outer chain (uniform per P block).
-enum : int { PJ_NONE = 0, PJ_MERGE_BW = 1, PJ_MERGE_AFF = 2, PJ_SEPARATE = 3 };
+// P(vX, .) as a segment from the row's left value vX, branch-free:
+//   g = { m: (vX & Am) ^ Bm,  x: vX & Ax,  a: vX * Ca + Da,  b: vX & Cb }
+// with per-operator constants (AND: m=vX; OR: m=~vX, x=vX; XOR: x=vX;
+// ADD: b=vX; SUB: a=-1, b=vX; MUL: a=vX), then composed in front of the
+// innermost outer segment s when that stays one LOP3+IMAD pair (g bitwise, or
+// s without a bitwise part), else s is the identity and the outer chain
+// starts at c[1].
+template <class W>
+struct PCoef {
+    W Am, Bm, Ax, Ca, Da, Cb;
+};
 
 template <class W>
-__device__ __forceinline__ Seg<W> first_seg(int pj, int pop, W s, const Seg<W> &so0)
+__device__ __forceinline__ PCoef<W> pcoef(int pop)
 {
-    Seg<W> g = seg_identity<W>();
+    const W Z = (W)0, O = (W)~(W)0, ONE = (W)1;
     switch (pop) {
-    case OP_AND: g.m = s; break;
-    case OP_OR: g.m = ~s; g.x = s; break;
-    case OP_XOR: g.x = s; break;
-    case OP_ADD: g.b = s; break;
-    case OP_SUB: g.a = (W)~(W)0; g.b = s; break;
-    default: g.a = s; break;  // MUL
+    case OP_AND: return PCoef<W>{O, Z, Z, Z, ONE, Z};
+    case OP_OR: return PCoef<W>{O, O, O, Z, ONE, Z};
+    case OP_XOR: return PCoef<W>{Z, O, O, Z, ONE, Z};
+    case OP_ADD: return PCoef<W>{Z, O, Z, Z, ONE, O};
+    case OP_SUB: return PCoef<W>{Z, O, Z, Z, O, O};
+    default: return PCoef<W>{Z, O, Z, ONE, Z, Z};  // MUL
     }
-    if (pj == PJ_MERGE_BW) {  // so0's bitwise part after g's
-        Seg<W> r = so0;
-        r.m = g.m & so0.m;
-        r.x = (g.x & so0.m) ^ so0.x;
-        return r;
-    }
-    if (pj == PJ_MERGE_AFF) {  // so0 has no bitwise part: A0 after g
-        Seg<W> r = so0;
-        r.b = so0.a * g.b + so0.b;
-        r.a = so0.a * g.a;
-        return r;
-    }
-    return g;  // PJ_SEPARATE
 }
 
-// Variant A: R2 >= 32, lanes over d2 (4 x 32 per step), rows d1 uniform.
+template <class W>
+__device__ __forceinline__ Seg<W> first_seg(const PCoef<W> &k, W vX, const Seg<W> &s)
+{
+    const W gm = (vX & k.Am) ^ k.Bm, gx = vX & k.Ax, ga = vX * k.Ca + k.Da, gb = vX & k.Cb;
+    return Seg<W>{gm & s.m, (gx & s.m) ^ s.x, s.a * ga, s.a * gb + s.b};
+}
+
+// Variant A: R2 >= 32, lanes over d2 (4 x 32 per step), rows uniform.
 // c[0] is rebuilt per row from the row's left value; c[1..NT-1] are fixed.
+// Rows are indexed relative to the unit's first row (32-bit).
 template <class W, int E, int NT>
-__device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop, int pj,
-                                     const Seg<W> &so0, const Seg<W> (&rest)[NT], const Seg<W> (&sl)[MAXSL], W y0,
-                                     XU xu, uint64_t ubase, uint32_t R2, uint32_t off2, uint64_t d1s, uint32_t d2s,
-                                     uint64_t u1, int lane, uint64_t &my_count)
+__device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
+                                     const PCoef<W> &kc, const Seg<W> &so0, const Seg<W> (&rest)[NT],
+                                     const Seg<W> (&sl)[MAXSL], W y0, XU xu, uint64_t ubase, uint32_t R2,
+                                     uint32_t off2, uint64_t d1s, uint32_t d2s, uint64_t u1, int lane,
+                                     uint64_t &my_count)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));  // example 0, sizes <= R0 (LDS)
@@ -319,29 +324,40 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
     for (int i = 0; i < MAXSL; ++i)
         slr[i] = sl[i];
     const Seg<W> s0 = so0;
-    uint32_t dlo = d2s;
-    uint64_t dy = 0, d1p = d1s;
+    const PCoef<W> k = kc;
+    const bool pnone = (pop == OP_NONE);
+    const uint64_t b0 = d1s * R2;
+    const uint32_t nrows = (uint32_t)((u1 - b0 + R2 - 1) / R2);
+    const uint32_t dlast = (uint32_t)(u1 - b0 - (uint64_t)(nrows - 1) * R2);
+    // left-input cursor of row d1s + rr
+    const W *gl = g0 + xu.off1 + d1s;
+    const W *gy = g0 + xu.offy;
+    const W *g1 = g0 + xu.off1;
+    const uint32_t R1p = (uint32_t)xu.R1p;
+    uint32_t dy = 0, d1p = 0;
     if (xu.x2d) {
-        dy = d1s / xu.R1p;
-        d1p = d1s - dy * xu.R1p;
+        dy = (uint32_t)(d1s / R1p);
+        d1p = (uint32_t)(d1s - (uint64_t)dy * R1p);
     }
-    W lnext = (W)0;
-    if (pop != OP_NONE)
-        lnext = left_input(g0, xu, dy, d1p);
+    auto left_at = [&](uint32_t rr) -> W {
+        if (xu.x2d)
+            return apply_bin<W>(xu.pxop, gy[dy], g1[d1p]);
+        return gl[rr];
+    };
+    W lnext = pnone ? (W)0 : left_at(0);
     const W *tr = t0 + off2 + lane;
-    for (uint64_t d1 = d1s;; ++d1, dlo = 0) {
-        const uint64_t row = d1 * R2;
-        if (row >= u1)
-            break;
-        const uint32_t dhi = (uint32_t)min((uint64_t)R2, u1 - row);
-        if (pop != OP_NONE) {
-            c[0] = first_seg(pj, pop, segs_apply(slr, lnext), s0);
-            if (row + R2 < u1) {  // prefetch the next row's left input
-                if (++d1p == xu.R1p && xu.x2d) {
+    uint32_t dlo = d2s;
+    for (uint32_t rr = 0; rr < nrows; ++rr, dlo = 0) {
+        const uint32_t dhi = (rr + 1 == nrows) ? dlast : R2;
+        const uint64_t d1 = d1s + rr;
+        if (!pnone) {
+            c[0] = first_seg(k, segs_apply(slr, lnext), s0);
+            if (rr + 1 < nrows) {  // prefetch the next row's left input
+                if (xu.x2d && ++d1p == R1p) {
                     d1p = 0;
                     ++dy;
                 }
-                lnext = left_input(g0, xu, dy, d1p);
+                lnext = left_at(rr + 1);
             }
         }
         for (uint32_t it = dlo; it < dhi; it += 128) {
@@ -357,8 +373,8 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
             const bool h3 = d2 + 96 < dhi && ((v3 ^ y0) & mask) == 0;
             if (__any_sync(FULL, h0 || h1 || h2 || h3)) {
                 const bool hk[4] = {h0, h1, h2, h3};
-                for (int k = 0; k < 4; ++k)
-                    on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, hk[k], d1, d2 + 32 * k, my_count);
+                for (int q = 0; q < 4; ++q)
+                    on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, hk[q], d1, d2 + 32 * q, my_count);
             }
         }
     }
@@ -449,7 +465,7 @@ struct SweepStats {
 
 template <class W, int E, int NT>
 __device__ __forceinline__ void dispatch_a_nt(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
-                                              int pj, const Seg<W> &so0, const Seg<W> (&chain)[8],
+                                              const PCoef<W> &kc, const Seg<W> &so0, const Seg<W> (&chain)[8],
                                               const Seg<W> (&sl)[MAXSL], W y0, const XU &xu, uint64_t ubase,
                                               uint32_t R2, uint32_t off2, uint64_t d1s, uint32_t d2s, uint64_t u1,
                                               int lane, uint64_t &cnt)
@@ -458,7 +474,7 @@ __device__ __forceinline__ void dispatch_a_nt(const KParams &p, const Staged &st
 #pragma unroll
     for (int i = 0; i < NT; ++i)
         rest[i] = chain[i];
-    sweep_a<W, E, NT>(p, st, od, pop, pj, so0, rest, sl, y0, xu, ubase, R2, off2, d1s, d2s, u1, lane, cnt);
+    sweep_a<W, E, NT>(p, st, od, pop, kc, so0, rest, sl, y0, xu, ubase, R2, off2, d1s, d2s, u1, lane, cnt);
 }
 
 template <class W, int E, int NT>
@@ -502,28 +518,30 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
     const uint32_t R2 = (uint32_t)t->T[prsz], off2 = t->toff[prsz];
     const uint64_t pb = od.pb;
     const bool early = (p.mode == SIMBA_MODE_SEARCH);
-    // variant A chain layout: c[0] = first segment (per row), c[1..] = rest
-    int pj = PJ_NONE;
+    // variant A chain layout: c[0] = first segment (per row), c[1..] = rest;
+    // s0 = the outer segment P merges into (identity when it cannot merge)
     Seg<W> chainA[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
         chainA[i] = seg_identity<W>();
     int ntA = 1;
+    Seg<W> s0 = seg_identity<W>();
+    PCoef<W> kc{};
     if (pop == OP_NONE) {
 #pragma unroll
         for (int i = 0; i < MAXSO; ++i)
             chainA[i] = so[i];
         ntA = nso > 1 ? nso : 1;
     } else {
+        kc = pcoef<W>(pop);
         const bool pbw = (pop == OP_AND || pop == OP_OR || pop == OP_XOR);
         if (nso > 0 && (pbw || !od.so0_bw)) {
-            pj = pbw ? PJ_MERGE_BW : PJ_MERGE_AFF;
+            s0 = so[0];
 #pragma unroll
             for (int i = 0; i < MAXSO; ++i)
                 chainA[i] = so[i];  // chainA[0] replaced per row
             ntA = nso;
         } else {
-            pj = PJ_SEPARATE;
 #pragma unroll
             for (int i = 0; i < MAXSO; ++i)
                 chainA[i + 1] = so[i];
@@ -576,16 +594,16 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
             const uint64_t u0 = n - ubase, u1 = stop - ubase;
             if (R2 >= 32) {
                 if (ntA <= 1)
-                    dispatch_a_nt<W, E, 1>(p, st, od, pop, pj, so[0], chainA, sl, y0, xu, ubase, R2, off2, d1s,
+                    dispatch_a_nt<W, E, 1>(p, st, od, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
                 else if (ntA == 2)
-                    dispatch_a_nt<W, E, 2>(p, st, od, pop, pj, so[0], chainA, sl, y0, xu, ubase, R2, off2, d1s,
+                    dispatch_a_nt<W, E, 2>(p, st, od, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
                 else if (ntA == 3)
-                    dispatch_a_nt<W, E, 3>(p, st, od, pop, pj, so[0], chainA, sl, y0, xu, ubase, R2, off2, d1s,
+                    dispatch_a_nt<W, E, 3>(p, st, od, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
                 else
-                    dispatch_a_nt<W, E, 5>(p, st, od, pop, pj, so[0], chainA, sl, y0, xu, ubase, R2, off2, d1s,
+                    dispatch_a_nt<W, E, 5>(p, st, od, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
             } else {
                 // lane chain: LEFT, P(., vR), OUTER with vR = this lane's d2 value
@@ -706,7 +724,7 @@ __device__ __forceinline__ void flush_counts(const KParams &p, uint64_t my_count
 }
 
 template <class W, int E>
-__global__ void __launch_bounds__(256, 2) unit_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
+__global__ void __launch_bounds__(512, 1) unit_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const Staged st = stage<W>(p, bi, smem, true);
@@ -762,7 +780,7 @@ __global__ void __launch_bounds__(256, 2) unit_kernel(const __grid_constant__ KP
 }
 
 template <class W>
-__global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
+__global__ void __launch_bounds__(512) direct_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const Staged st = stage<W>(p, bi, smem, false);
@@ -1295,8 +1313,10 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     int R0 = o.r0;
     if (R0 == 0) {
         R0 = 1;
+        // largest shared-memory table up to 160 KB: longer rows and fewer
+        // units beat a second CTA per SM (occupancy is register-bound anyway)
         for (int r = 2; r <= max_size; ++r) {
-            if (t.T[r] > 65535 || tbl_size(r) * c->wbytes > 64 * 1024)
+            if (t.T[r] > 65535 || (tbl_size(r) + 128) * c->wbytes > 160 * 1024)
                 break;
             R0 = r;
         }
@@ -1344,9 +1364,12 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->tbl_bytes = pad16((uint64_t)(c->tbl_len + 128) * c->wbytes);  // +128: unrolled reads past a row
     c->ex_bytes = pad16((uint64_t)n * (k + 1) * c->wbytes);
     c->stage_examples = c->ex_bytes <= 32 * 1024;
-    c->block_threads = o.block_threads ? o.block_threads : 256;
-    if (c->block_threads % 32 || c->block_threads < 32 || c->block_threads > 256)
-        return bail(fail(SIMBA_EINVAL, "block_threads must be a multiple of 32 in 32..256"));
+    // 16 warps per SM either way (128 registers per thread): one 512-thread CTA
+    // when the shared-memory tables do not leave room for two
+    c->block_threads = o.block_threads ? o.block_threads
+                                       : ((sizeof(Tabs) + c->tbl_bytes + c->ex_bytes > 100 * 1024) ? 512 : 256);
+    if (c->block_threads % 32 || c->block_threads < 32 || c->block_threads > 512)
+        return bail(fail(SIMBA_EINVAL, "block_threads must be a multiple of 32 in 32..512"));
     c->lvl_off = (uint32_t)(sizeof(Tabs) + c->tbl_bytes + (c->stage_examples ? c->ex_bytes : 0));
     {
         size_t lv = 0;

@@ -176,9 +176,12 @@ class DeviceContext:
         self.table = build(spec.k, max_size)
 
     def close(self):
-        if getattr(self, "_ptr", None):
-            N.lib.simba_ctx_destroy(self._ptr)
+        ptr = getattr(self, "_ptr", None)
+        if ptr:
             self._ptr = None
+            lib = getattr(N, "lib", None)  # None during interpreter shutdown
+            if lib is not None:
+                lib.simba_ctx_destroy(ptr)
 
     def __enter__(self):
         return self

@@ -25,6 +25,13 @@ def run(label, spec, sizes, **kw):
                   f"rank_units={r.rank_units} ctx={tc*1e3:.0f}ms {info}", flush=True)
 
 spec4 = unsat(4, 32, 10, 31337)
+if len(sys.argv) > 1 and sys.argv[1] == "r0":
+    run("C5 r0=5 256x2", spec4, [11, 12, 13])
+    run("C5 r0=5 512x1", spec4, [11, 12, 13], block_threads=512)
+    run("C5 r0=6 512x1", spec4, [11, 12, 13], r0=6, block_threads=512)
+    run("C3 r0=6 256x2", unsat(3, 32, 10, 777), [11, 12])
+    run("C3 r0=7 512x1", unsat(3, 32, 10, 777), [11, 12], r0=7, block_threads=512)
+    sys.exit()
 if len(sys.argv) > 1:
     run("C5 unit", spec4, [int(a) for a in sys.argv[1:]]); sys.exit()
 run("C5 unit", spec4, [9, 10, 11, 12, 13])

@@ -153,15 +153,17 @@ def test_counts_independent_of_kernel_configuration(variant):
 # ---------------------------------------------------------------- rank windows (C5 sizes 11..13)
 
 
-# exercise both a large global table and the minimal one on the C5 windows
-WINDOW_RG = {"C5_s12_t1": 5, "C5dense_s13_op2": 5, "C5dense_s12_op4": 9, "C5_s13_t0": 9}
+# exercise (r0, rg) combinations other than the automatic one on some C5 windows
+WINDOW_RG = {"C5_s12_t1": (5, 5), "C5dense_s13_op2": (6, 6), "C5dense_s12_op4": (4, 9), "C5_s13_t0": (6, 9),
+             "C5dense_s11_op4": (3, 7)}
 
 
 @pytest.mark.parametrize("name", [r["name"] for r in load_golden("windows")])
 def test_windows_match_reference(name):
     r = [r for r in load_golden("windows") if r["name"] == name][0]
     spec = spec_of(r["spec"])
-    with DeviceContext(spec, r["size_bound"], rg=WINDOW_RG.get(r["name"], 0)) as ctx:
+    r0, rg = WINDOW_RG.get(r["name"], (0, 0))
+    with DeviceContext(spec, r["size_bound"], r0=r0, rg=rg) as ctx:
         c = ctx.count(r["size"], r["lo"], r["hi"])
         assert (c.count, c.best_rank) == (r["count"], r["first"])
         assert c.visited == r["hi"] - r["lo"]
