@@ -360,8 +360,26 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
                 lnext = left_at(rr + 1);
             }
         }
-        for (uint32_t it = dlo; it < dhi; it += 128) {
-            // the shared table is padded by 128 words: reads past a row are harmless
+        uint32_t it = dlo;
+        // full steps: 8 x 32 candidates, no bounds predicates
+        for (; it + 256 <= dhi; it += 256) {
+            W v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                v[q] = chain_apply(c, tr[it + 32 * q]);
+            bool any = false;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                any |= ((v[q] ^ y0) & mask) == 0;
+            if (__any_sync(FULL, any)) {
+                for (int q = 0; q < 8; ++q)
+                    on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, ((v[q] ^ y0) & mask) == 0, d1,
+                                  it + lane + 32 * q, my_count);
+            }
+        }
+        // tail: 4 x 32 with bounds (the shared table is padded by 128 words,
+        // so reads past a row are harmless)
+        for (; it < dhi; it += 128) {
             const W v0 = chain_apply(c, tr[it]);
             const W v1 = chain_apply(c, tr[it + 32]);
             const W v2 = chain_apply(c, tr[it + 64]);
@@ -383,8 +401,39 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
 // Variant B: R2 < 32, lanes over (row, d2) pairs (G = 32 / R2 rows per step,
 // 4 steps per iteration); the lane's chain LEFT, P(., vR), OUTER is fixed and
 // its input is the row's left input (one table read, or two combined by N_X's
-// operator for a two-digit X).  All per-candidate index math is 32-bit and
-// relative to the unit's first row; the chain lives in registers.
+// operator for a two-digit X).  Per-lane pointer cursors step through the
+// global table; the row bounds are 32-bit and relative to the unit's first row.
+template <class W>
+__device__ __forceinline__ void bin4(int op, const W (&a)[4], const W (&b)[4], W (&r)[4])
+{
+    switch (op) {
+    case OP_AND:
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = a[k] & b[k];
+        break;
+    case OP_OR:
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = a[k] | b[k];
+        break;
+    case OP_XOR:
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = a[k] ^ b[k];
+        break;
+    case OP_ADD:
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = a[k] + b[k];
+        break;
+    case OP_SUB:
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = a[k] - b[k];
+        break;
+    default:
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = a[k] * b[k];
+        break;
+    }
+}
+
 template <class W, int E, int NT, bool X2D>
 __device__ __noinline__ void sweep_b(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
                                      const Seg<W> (&cin)[NT], W y0, XU xu, uint64_t ubase, uint32_t R2, uint32_t off2,
@@ -405,39 +454,51 @@ __device__ __noinline__ void sweep_b(const KParams &p, const Staged &st, const O
     const uint32_t d2first = (uint32_t)(u0 - b0);                   // first row starts here
     const uint32_t d2last = (uint32_t)(u1 - b0 - (uint64_t)(nrows - 1) * R2);  // last row ends before
     const bool pnone = (pop == OP_NONE);
-    // row cursor: !X2D: row value gl[rr];  X2D: (dy, d1p) of row d1s + rr
-    const W *gl = g0 + xu.off1 + d1s;
-    const W *gy = g0 + xu.offy;
-    const W *g1 = g0 + xu.off1;
-    uint32_t dy = 0, d1p = 0, qG = 0, rG = 0;
-    const uint32_t R1p = (uint32_t)xu.R1p;
+    const int pxop = xu.pxop;
+    // cursors: !X2D: pl -> G[L1][d1s + rr];  X2D: py -> G[Y][dy], p1 -> G[L1][d1p]
+    const W *pl = g0 + xu.off1 + d1s + lg;
+    const W *py = g0 + xu.offy;
+    const W *p1 = g0 + xu.off1;
+    const W *p1end = g0 + xu.off1 + xu.R1p;
+    uint32_t qG = 0, rG = 0;
     if constexpr (X2D) {
+        const uint32_t R1p = (uint32_t)xu.R1p;
         const uint64_t r0 = d1s + lg;
-        dy = (uint32_t)(r0 / R1p);
-        d1p = (uint32_t)(r0 - (uint64_t)dy * R1p);
+        const uint64_t dy = r0 / R1p;
+        py += dy;
+        p1 += r0 - dy * R1p;
         qG = G / R1p;
         rG = G - qG * R1p;
     }
     for (uint32_t rb = 0; rb < nrows; rb += 4 * G) {
-        bool h[4], act[4];
+        bool act[4];
         W in[4];
+        if constexpr (X2D) {
+            W a[4], bv[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t rr = rb + k * G + lg;
-            act[k] = lane_ok && rr < nrows && (rr != 0 || ld2 >= d2first) && (rr + 1 != nrows || ld2 < d2last);
-            if constexpr (X2D) {
-                const W a = gy[act[k] ? dy : 0], bb = g1[act[k] ? d1p : 0];
-                in[k] = apply_bin<W>(xu.pxop, a, bb);
-                d1p += rG;
-                dy += qG;
-                if (d1p >= R1p) {
-                    d1p -= R1p;
-                    ++dy;
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t rr = rb + k * G + lg;
+                act[k] = lane_ok && rr < nrows && (rr != 0 || ld2 >= d2first) && (rr + 1 != nrows || ld2 < d2last);
+                a[k] = act[k] ? *py : (W)0;
+                bv[k] = act[k] ? *p1 : (W)0;
+                p1 += rG;
+                py += qG;
+                if (p1 >= p1end) {
+                    p1 -= xu.R1p;
+                    ++py;
                 }
-            } else {
-                in[k] = pnone ? (W)0 : gl[act[k] ? rr : 0];
             }
+            bin4<W>(pxop, a, bv, in);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t rr = rb + k * G + lg;
+                act[k] = lane_ok && rr < nrows && (rr != 0 || ld2 >= d2first) && (rr + 1 != nrows || ld2 < d2last);
+                in[k] = (act[k] && !pnone) ? pl[k * G] : (W)0;
+            }
+            pl += 4 * G;
         }
+        bool h[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const W v = chain_apply(c, in[k]);
