@@ -206,10 +206,18 @@ def main():
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if world != args.gpus and "WORLD_SIZE" in os.environ:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    # SIMBA_BENCH_DEVICE / SIMBA_BENCH_BACKEND=gloo: exercise the multi-rank
+    # path with several ranks on one GPU (testing only; NCCL needs distinct GPUs)
+    local = env_int("SIMBA_BENCH_DEVICE", local)
+    backend = os.environ.get("SIMBA_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    rdev = dev if backend == "nccl" else torch.device("cpu")  # reduction tensors
 
     C = args.size_bound
     spec = S.Specification(k=K, w=W_BITS, pairs=unsat_pairs())
@@ -224,7 +232,7 @@ def main():
     def allmax(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -243,9 +251,9 @@ def main():
             ex0[s] = r.ex0_hits
             levels.append((s, r))
         if world > 1:  # exchange: SUM(count, visited), MIN(first) for all levels at once
-            cnt = torch.tensor([[r.count, r.visited] for _, r in levels], dtype=torch.int64, device=dev)
+            cnt = torch.tensor([[r.count, r.visited] for _, r in levels], dtype=torch.int64, device=rdev)
             fst = torch.tensor([r.best_rank if r.best_rank is not None else (1 << 63) - 1 for _, r in levels],
-                               dtype=torch.int64, device=dev)
+                               dtype=torch.int64, device=rdev)
             dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
             dist.all_reduce(fst, op=dist.ReduceOp.MIN)
             tot_visited = int(cnt[:, 1].sum().item())
@@ -301,7 +309,7 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             c2 = DeviceContext(spec, C, device=local)
-            parallel.count_levels(parallel.device_scan(c2), totals, rank, world, device=dev)
+            parallel.count_levels(parallel.device_scan(c2), totals, rank, world, device=rdev)
             hb, db = c2.copied_bytes()
             h2d += hb
             d2h += db

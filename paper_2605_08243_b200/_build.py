@@ -23,18 +23,18 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and OUT.exists() and all(OUT.stat().st_mtime >= p.stat().st_mtime for p in DEPS):
-        return OUT
-    OUT.parent.mkdir(parents=True, exist_ok=True)
-    tmp = OUT.with_suffix(".so.tmp")
+def build(force: bool = False, verbose: bool = False, out: Path = OUT, defines=()) -> Path:
+    if not force and out.exists() and all(out.stat().st_mtime >= p.stat().st_mtime for p in DEPS):
+        return out
+    out.parent.mkdir(parents=True, exist_ok=True)
+    tmp = out.with_suffix(".so.tmp")
     cmd = [nvcc(), "-shared", "-Xcompiler", "-fPIC", *ARCH, "-O3", "-lineinfo", "-std=c++17",
-           "-I", str(ROOT / "include"), "-o", str(tmp), *map(str, SRC)]
+           "-I", str(ROOT / "include"), *[f"-D{d}" for d in defines], "-o", str(tmp), *map(str, SRC)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)
-    tmp.replace(OUT)
-    return OUT
+    tmp.replace(out)
+    return out
 
 
 if __name__ == "__main__":

@@ -11,8 +11,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
+import os
+
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "_lib" / "libsimba.so"
+LIB_PATH = Path(os.environ.get("SIMBA_LIB", PKG / "_lib" / "libsimba.so"))
 
 OK, EINVAL, ERANGE, ECAPACITY, ECUDA, ENOMEM = 0, 1, 2, 3, 4, 5
 MAX_SIZE = 24

@@ -784,8 +784,12 @@ __device__ __forceinline__ void flush_counts(const KParams &p, uint64_t my_count
     }
 }
 
+#ifndef SIMBA_UNIT_THREADS
+#define SIMBA_UNIT_THREADS 512
+#endif
+
 template <class W, int E>
-__global__ void __launch_bounds__(512, 1) unit_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
+__global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const Staged st = stage<W>(p, bi, smem, true);
@@ -841,7 +845,7 @@ __global__ void __launch_bounds__(512, 1) unit_kernel(const __grid_constant__ KP
 }
 
 template <class W>
-__global__ void __launch_bounds__(512) direct_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
+__global__ void __launch_bounds__(SIMBA_UNIT_THREADS) direct_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const Staged st = stage<W>(p, bi, smem, false);
@@ -1428,9 +1432,11 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     // 16 warps per SM either way (128 registers per thread): one 512-thread CTA
     // when the shared-memory tables do not leave room for two
     c->block_threads = o.block_threads ? o.block_threads
-                                       : ((sizeof(Tabs) + c->tbl_bytes + c->ex_bytes > 100 * 1024) ? 512 : 256);
-    if (c->block_threads % 32 || c->block_threads < 32 || c->block_threads > 512)
-        return bail(fail(SIMBA_EINVAL, "block_threads must be a multiple of 32 in 32..512"));
+                                       : ((sizeof(Tabs) + c->tbl_bytes + c->ex_bytes > 100 * 1024)
+                                              ? SIMBA_UNIT_THREADS
+                                              : (SIMBA_UNIT_THREADS > 256 ? SIMBA_UNIT_THREADS / 2 : 256));
+    if (c->block_threads % 32 || c->block_threads < 32 || c->block_threads > SIMBA_UNIT_THREADS)
+        return bail(fail(SIMBA_EINVAL, "block_threads must be a multiple of 32 in 32..%d", SIMBA_UNIT_THREADS));
     c->lvl_off = (uint32_t)(sizeof(Tabs) + c->tbl_bytes + (c->stage_examples ? c->ex_bytes : 0));
     {
         size_t lv = 0;

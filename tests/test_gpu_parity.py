@@ -181,6 +181,19 @@ def test_windows_match_reference(name):
         assert tot == r["count"] and (min(first) if first else None) == r["first"]
 
 
+def test_sharded_search_min_equals_unsharded():
+    # each shard's early-exit search returns its exact minimum,
+    # so the MIN over shards is the level minimum (the reference's rank)
+    for r in [r for r in load_golden("windows") if r["count"] > 1][:8]:
+        spec = spec_of(r["spec"])
+        with DeviceContext(spec, r["size_bound"]) as ctx:
+            for nsh in (2, 3, 5):
+                got = [ctx.run(r["size"], r["lo"], r["hi"], mode="search", chunk=1 << 10, shard=i, nshards=nsh)
+                       for i in range(nsh)]
+                firsts = [g.best_rank for g in got if g.best_rank is not None]
+                assert min(firsts) == r["first"], (r["name"], nsh)
+
+
 def test_scan_range_seam_matches_reference_chunks():
     r = [r for r in load_golden("counts") if r["name"] == "dense_k3_w3_n2"][0]
     spec = spec_of(r["spec"])
