@@ -226,7 +226,7 @@ __device__ __forceinline__ W left_input(const W *g, const XU &xu, uint64_t dy, u
 // then verify the survivors against every example with the reference-exact
 // evaluator (decode_tokens + eval_rpn).
 template <class W, int E>
-__device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop, XU xu,
+__device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop, XU xu,
                                      uint64_t ubase, uint32_t R2, uint32_t off2, bool hit, uint64_t d1, uint32_t d2,
                                      uint64_t &my_count)
 {
@@ -240,10 +240,14 @@ __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const O
     const uint64_t d1p = xu.x2d ? d1 - dy * xu.R1p : d1;
 #pragma unroll
     for (int e = 1; e < E; ++e) {
-        Seg<W> so[MAXSO], sl[MAXSL];
-        bcast_seg_array<W, MAXSO>(od.so, e, so);
-        bcast_seg_array<W, MAXSL>(od.sl, e, sl);
         if (hit) {
+            Seg<W> so[MAXSO], sl[MAXSL];
+#pragma unroll
+            for (int i = 0; i < MAXSO; ++i)
+                so[i] = sx->so[e][i];
+#pragma unroll
+            for (int i = 0; i < MAXSL; ++i)
+                sl[i] = sx->sl[e][i];
             const W *te = gtbl + (size_t)e * p.gtbl_len;
             const W vR = te[off2 + d2];
             W v = vR;
@@ -302,11 +306,89 @@ __device__ __forceinline__ Seg<W> first_seg(const PCoef<W> &k, W vX, const Seg<W
     return Seg<W>{gm & s.m, (gx & s.m) ^ s.x, s.a * ga, s.a * gb + s.b};
 }
 
-// Variant A: R2 >= 32, lanes over d2 (4 x 32 per step), rows uniform.
-// c[0] is rebuilt per row from the row's left value; c[1..NT-1] are fixed.
-// Rows are indexed relative to the unit's first row (32-bit).
+// Final-segment folding.  If the last chain segment L = v -> a*((v&m)^x)+b
+// has an odd multiplier a it is a bijection mod 2^w on (v & m), so
+//   L(v) == y0 (mod 2^w)  <=>  ((v & (m & mask)) ^ (((y0 - b) * a^-1 ^ x) & mask)) == 0
+// -- the same candidate-exact predicate, one LOP3 on L's input instead of a
+// LOP3 + IMAD + compare on its output.  Even a: no folding (tm = mask, tc = y0).
+template <class W>
+__device__ __forceinline__ W modinv_odd(W a)
+{
+    W x = a;  // a*a == 1 (mod 8) for odd a: 3 correct bits, Newton doubles them
+#pragma unroll
+    for (int i = 0; i < (sizeof(W) == 4 ? 4 : 5); ++i)
+        x = x * ((W)2 - a * x);
+    return x;
+}
+
+template <class W>
+__device__ __forceinline__ bool fold_last(const Seg<W> &L, W y0, W mask, W &tm, W &tc)
+{
+#ifdef SIMBA_NO_FOLD
+    return false;
+#endif
+    if (!(L.a & (W)1))
+        return false;
+    tm = L.m & mask;
+    tc = (((y0 - L.b) * modinv_odd(L.a)) ^ L.x) & mask;
+    return true;
+}
+
+template <class W, int K, int N>
+__device__ __forceinline__ W chain_k(const Seg<W> (&c)[N], W v)
+{
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+        v = seg_apply(c[i], v);
+    return v;
+}
+
+// One row of variant A: d2 in [dlo, dhi), value chain c[0..K-1] then the
+// masked test ((v & tm) ^ tc) == 0.
+template <class W, int E, int K, int N>
+__device__ __forceinline__ void row_sweep(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
+                                          const XU &xu, uint64_t ubase, uint32_t R2, uint32_t off2,
+                                          const Seg<W> (&c)[N], W tm, W tc, const W *tr, int lane, uint32_t dlo,
+                                          uint32_t dhi, uint64_t d1, uint64_t &my_count)
+{
+    uint32_t it = dlo;
+    // full steps: 8 x 32 candidates, no bounds predicates
+    for (; it + 256 <= dhi; it += 256) {
+        W v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            v[q] = chain_k<W, K>(c, tr[it + 32 * q]);
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            any |= ((v[q] & tm) ^ tc) == 0;
+        if (__any_sync(FULL, any)) {
+            for (int q = 0; q < 8; ++q)
+                on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, ((v[q] & tm) ^ tc) == 0, d1, it + lane + 32 * q,
+                              my_count);
+        }
+    }
+    // tail: 4 x 32 with bounds (the shared table is padded by 128 words,
+    // so reads past a row are harmless)
+    for (; it < dhi; it += 128) {
+        bool h[4];
+        const uint32_t d2 = it + lane;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            h[q] = d2 + 32 * q < dhi && ((chain_k<W, K>(c, tr[it + 32 * q]) & tm) ^ tc) == 0;
+        if (__any_sync(FULL, h[0] || h[1] || h[2] || h[3])) {
+            for (int q = 0; q < 4; ++q)
+                on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h[q], d1, d2 + 32 * q, my_count);
+        }
+    }
+}
+
+// Variant A: R2 >= 32, lanes over d2, rows uniform.  c[0] is rebuilt per row
+// from the row's left value; c[1..NT-1] are fixed.  The last segment is folded
+// into the test (per row when NT == 1, once per call otherwise).  Rows are
+// indexed relative to the unit's first row (32-bit).
 template <class W, int E, int NT>
-__device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
+__device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
                                      const PCoef<W> &kc, const Seg<W> &so0, const Seg<W> (&rest)[NT],
                                      const Seg<W> (&sl)[MAXSL], W y0, XU xu, uint64_t ubase, uint32_t R2,
                                      uint32_t off2, uint64_t d1s, uint32_t d2s, uint64_t u1, int lane,
@@ -316,6 +398,7 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
     const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));  // example 0, sizes <= R0 (LDS)
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);               // example 0, sizes <= RG (global)
     const W mask = (W)p.mask;
+    const W y0m = y0 & mask;
     Seg<W> c[NT], slr[MAXSL];
 #pragma unroll
     for (int i = 0; i < NT; ++i)
@@ -326,6 +409,10 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
     const Seg<W> s0 = so0;
     const PCoef<W> k = kc;
     const bool pnone = (pop == OP_NONE);
+    W tmF = mask, tcF = y0m;
+    bool foldF = false;
+    if constexpr (NT >= 2)
+        foldF = fold_last(c[NT - 1], y0m, mask, tmF, tcF);
     const uint64_t b0 = d1s * R2;
     const uint32_t nrows = (uint32_t)((u1 - b0 + R2 - 1) / R2);
     const uint32_t dlast = (uint32_t)(u1 - b0 - (uint64_t)(nrows - 1) * R2);
@@ -360,40 +447,20 @@ __device__ __noinline__ void sweep_a(const KParams &p, const Staged &st, const O
                 lnext = left_at(rr + 1);
             }
         }
-        uint32_t it = dlo;
-        // full steps: 8 x 32 candidates, no bounds predicates
-        for (; it + 256 <= dhi; it += 256) {
-            W v[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                v[q] = chain_apply(c, tr[it + 32 * q]);
-            bool any = false;
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                any |= ((v[q] ^ y0) & mask) == 0;
-            if (__any_sync(FULL, any)) {
-                for (int q = 0; q < 8; ++q)
-                    on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, ((v[q] ^ y0) & mask) == 0, d1,
-                                  it + lane + 32 * q, my_count);
-            }
-        }
-        // tail: 4 x 32 with bounds (the shared table is padded by 128 words,
-        // so reads past a row are harmless)
-        for (; it < dhi; it += 128) {
-            const W v0 = chain_apply(c, tr[it]);
-            const W v1 = chain_apply(c, tr[it + 32]);
-            const W v2 = chain_apply(c, tr[it + 64]);
-            const W v3 = chain_apply(c, tr[it + 96]);
-            const uint32_t d2 = it + lane;
-            const bool h0 = d2 < dhi && ((v0 ^ y0) & mask) == 0;
-            const bool h1 = d2 + 32 < dhi && ((v1 ^ y0) & mask) == 0;
-            const bool h2 = d2 + 64 < dhi && ((v2 ^ y0) & mask) == 0;
-            const bool h3 = d2 + 96 < dhi && ((v3 ^ y0) & mask) == 0;
-            if (__any_sync(FULL, h0 || h1 || h2 || h3)) {
-                const bool hk[4] = {h0, h1, h2, h3};
-                for (int q = 0; q < 4; ++q)
-                    on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, hk[q], d1, d2 + 32 * q, my_count);
-            }
+        if constexpr (NT == 1) {
+            W tm, tc;
+            if (fold_last(c[0], y0m, mask, tm, tc))
+                row_sweep<W, E, 0>(p, st, sx, pop, xu, ubase, R2, off2, c, tm, tc, tr, lane, dlo, dhi, d1, my_count);
+            else
+                row_sweep<W, E, 1>(p, st, sx, pop, xu, ubase, R2, off2, c, mask, y0m, tr, lane, dlo, dhi, d1,
+                                   my_count);
+        } else {
+            if (foldF)
+                row_sweep<W, E, NT - 1>(p, st, sx, pop, xu, ubase, R2, off2, c, tmF, tcF, tr, lane, dlo, dhi, d1,
+                                        my_count);
+            else
+                row_sweep<W, E, NT>(p, st, sx, pop, xu, ubase, R2, off2, c, mask, y0m, tr, lane, dlo, dhi, d1,
+                                    my_count);
         }
     }
 }
@@ -435,12 +502,12 @@ __device__ __forceinline__ void bin4(int op, const W (&a)[4], const W (&b)[4], W
 }
 
 template <class W, int E, int NT, bool X2D>
-__device__ __noinline__ void sweep_b(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
-                                     const Seg<W> (&cin)[NT], W y0, XU xu, uint64_t ubase, uint32_t R2, uint32_t off2,
-                                     uint64_t d1s, uint64_t u0, uint64_t u1, int lane, uint64_t &my_count)
+__device__ __noinline__ void sweep_b(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
+                                     const Seg<W> (&cin)[NT], W tm, W tc, XU xu, uint64_t ubase, uint32_t R2,
+                                     uint32_t off2, uint64_t d1s, uint64_t u0, uint64_t u1, int lane,
+                                     uint64_t &my_count)
 {
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);
-    const W mask = (W)p.mask;
     Seg<W> c[NT];
 #pragma unroll
     for (int i = 0; i < NT; ++i)
@@ -500,13 +567,11 @@ __device__ __noinline__ void sweep_b(const KParams &p, const Staged &st, const O
         }
         bool h[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const W v = chain_apply(c, in[k]);
-            h[k] = act[k] && ((v ^ y0) & mask) == 0;
-        }
+        for (int k = 0; k < 4; ++k)
+            h[k] = act[k] && ((chain_apply(c, in[k]) & tm) ^ tc) == 0;
         if (__any_sync(FULL, h[0] || h[1] || h[2] || h[3])) {
             for (int k = 0; k < 4; ++k)
-                on_hits<W, E>(p, st, od, pop, xu, ubase, R2, off2, h[k], h[k] ? d1s + rb + k * G + lg : 0, ld2,
+                on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h[k], h[k] ? d1s + rb + k * G + lg : 0, ld2,
                               my_count);
         }
     }
@@ -525,7 +590,7 @@ struct SweepStats {
 };
 
 template <class W, int E, int NT>
-__device__ __forceinline__ void dispatch_a_nt(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
+__device__ __forceinline__ void dispatch_a_nt(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
                                               const PCoef<W> &kc, const Seg<W> &so0, const Seg<W> (&chain)[8],
                                               const Seg<W> (&sl)[MAXSL], W y0, const XU &xu, uint64_t ubase,
                                               uint32_t R2, uint32_t off2, uint64_t d1s, uint32_t d2s, uint64_t u1,
@@ -535,12 +600,12 @@ __device__ __forceinline__ void dispatch_a_nt(const KParams &p, const Staged &st
 #pragma unroll
     for (int i = 0; i < NT; ++i)
         rest[i] = chain[i];
-    sweep_a<W, E, NT>(p, st, od, pop, kc, so0, rest, sl, y0, xu, ubase, R2, off2, d1s, d2s, u1, lane, cnt);
+    sweep_a<W, E, NT>(p, st, sx, pop, kc, so0, rest, sl, y0, xu, ubase, R2, off2, d1s, d2s, u1, lane, cnt);
 }
 
 template <class W, int E, int NT>
-__device__ __forceinline__ void dispatch_b_nt(const KParams &p, const Staged &st, const Odometer<W, E> &od, int pop,
-                                              const Seg<W> (&chain)[8], W y0, const XU &xu, uint64_t ubase,
+__device__ __forceinline__ void dispatch_b_nt(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
+                                              const Seg<W> (&chain)[8], W tm, W tc, const XU &xu, uint64_t ubase,
                                               uint32_t R2, uint32_t off2, uint64_t d1s, uint64_t u0, uint64_t u1,
                                               int lane, uint64_t &cnt)
 {
@@ -549,9 +614,9 @@ __device__ __forceinline__ void dispatch_b_nt(const KParams &p, const Staged &st
     for (int i = 0; i < NT; ++i)
         c[i] = chain[i];
     if (xu.x2d)
-        sweep_b<W, E, NT, true>(p, st, od, pop, c, y0, xu, ubase, R2, off2, d1s, u0, u1, lane, cnt);
+        sweep_b<W, E, NT, true>(p, st, sx, pop, c, tm, tc, xu, ubase, R2, off2, d1s, u0, u1, lane, cnt);
     else
-        sweep_b<W, E, NT, false>(p, st, od, pop, c, y0, xu, ubase, R2, off2, d1s, u0, u1, lane, cnt);
+        sweep_b<W, E, NT, false>(p, st, sx, pop, c, tm, tc, xu, ubase, R2, off2, d1s, u0, u1, lane, cnt);
 }
 
 // All ranks [n, n1) of one P block (n1 <= pend).  The outer chain and P's
@@ -560,9 +625,18 @@ __device__ __forceinline__ void dispatch_b_nt(const KParams &p, const Staged &st
 // level).  Returns the first rank not scanned (n1 unless a search hit allows
 // early exit).
 template <class W, int E>
-__device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, Odometer<W, E> &od, uint64_t n,
-                                            uint64_t n1, int lane, SweepStats &ss)
+__device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &st, Odometer<W, E> &od, uint64_t n,
+                                               uint64_t n1, int lane, SweepStats &ss)
 {
+    SegStash<W, E> *sx = &od.L->stash;
+    if constexpr (E > 1) {
+        if (lane < E) {
+#pragma unroll
+            for (int i = 0; i < MAXSO; ++i)
+                sx->so[lane][i] = od.so[i];
+        }
+        __syncwarp();
+    }
     extern __shared__ __align__(16) unsigned char smem[];
     const Tabs *t = stabs();
     const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));
@@ -623,8 +697,17 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
             const uint64_t rel = n - pb;
             const uint64_t q = div_T(t, prsz, rel);
             d2s = (uint32_t)(rel - q * R2);
-            if (!od.have_x || q >= od.qend)
+            if (!od.have_x || q >= od.qend) {
                 od.decode_x(q);
+                if constexpr (E > 1) {
+                    if (lane < E) {
+#pragma unroll
+                        for (int i = 0; i < MAXSL; ++i)
+                            sx->sl[lane][i] = od.sl[i];
+                    }
+                    __syncwarp();
+                }
+            }
             xu.x2d = od.x2d ? 1 : 0;
             xu.sz1 = od.sz1;
             xu.off1 = t->toff[od.sz1];
@@ -655,16 +738,16 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
             const uint64_t u0 = n - ubase, u1 = stop - ubase;
             if (R2 >= 32) {
                 if (ntA <= 1)
-                    dispatch_a_nt<W, E, 1>(p, st, od, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
+                    dispatch_a_nt<W, E, 1>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
                 else if (ntA == 2)
-                    dispatch_a_nt<W, E, 2>(p, st, od, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
+                    dispatch_a_nt<W, E, 2>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
                 else if (ntA == 3)
-                    dispatch_a_nt<W, E, 3>(p, st, od, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
+                    dispatch_a_nt<W, E, 3>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
                 else
-                    dispatch_a_nt<W, E, 5>(p, st, od, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
+                    dispatch_a_nt<W, E, 5>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
                                            d2s, u1, lane, ss.count);
             } else {
                 // lane chain: LEFT, P(., vR), OUTER with vR = this lane's d2 value
@@ -682,15 +765,26 @@ __device__ __noinline__ uint64_t run_pblock(const KParams &p, const Staged &st, 
                 }
                 for (int i = 0; i < nso; ++i)
                     ch.then_seg(so[i]);
-                const int nt = (int)__reduce_max_sync(FULL, (unsigned)ch.n);
-                if (nt <= 2)
-                    dispatch_b_nt<W, E, 2>(p, st, od, pop, ch.s, y0, xu, ubase, R2, off2, d1s, u0, u1, lane,
+                // fold this lane's last segment into the test when invertible
+                const W mask = (W)p.mask;
+                W tm = mask, tc = y0 & mask;
+                int nl = ch.n;
+                if (nl > 0 && fold_last(ch.last(), (W)(y0 & mask), mask, tm, tc)) {
+                    ch.set_last(seg_identity<W>());
+                    --nl;
+                }
+                const int nt = (int)__reduce_max_sync(FULL, (unsigned)nl);
+                if (nt == 0)
+                    dispatch_b_nt<W, E, 1>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, d1s, u0, u1, lane,
+                                           ss.count);
+                else if (nt <= 2)
+                    dispatch_b_nt<W, E, 2>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, d1s, u0, u1, lane,
                                            ss.count);
                 else if (nt <= 4)
-                    dispatch_b_nt<W, E, 4>(p, st, od, pop, ch.s, y0, xu, ubase, R2, off2, d1s, u0, u1, lane,
+                    dispatch_b_nt<W, E, 4>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, d1s, u0, u1, lane,
                                            ss.count);
                 else
-                    dispatch_b_nt<W, E, 8>(p, st, od, pop, ch.s, y0, xu, ubase, R2, off2, d1s, u0, u1, lane,
+                    dispatch_b_nt<W, E, 8>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, d1s, u0, u1, lane,
                                            ss.count);
             }
         }

@@ -543,10 +543,19 @@ struct LevelStack {
     W sib[MAXLV][E];       // left sibling value per example (binary levels)
 };
 
+// per-example chain segments of the current unit, for the rare multi-example
+// hit refinement (lane e writes example e's segments)
+template <class W, int E>
+struct SegStash {
+    Seg<W> so[E][MAXSO];
+    Seg<W> sl[E][MAXSL];
+};
+
 template <class W, int E>
 struct WarpLevels {
     LevelStack<W, E> outer;
     LevelStack<W, E> xs;
+    SegStash<W, E> stash;
 };
 
 template <class W, int E>
@@ -621,7 +630,7 @@ struct Odometer {
             st.sib[i][lane] = sib;
     }
 
-    __device__ __noinline__ void decode_outer(uint64_t n)
+    __device__ __forceinline__ void decode_outer(uint64_t n)
     {
         const Tabs *t = stabs();
         LevelStack<W, E> &st = L->outer;
@@ -672,7 +681,7 @@ struct Odometer {
         nx = 0;
     }
 
-    __device__ __noinline__ void decode_x(uint64_t q)
+    __device__ __forceinline__ void decode_x(uint64_t q)
     {
         const Tabs *t = stabs();
         LevelStack<W, E> &st = L->xs;
