@@ -248,3 +248,20 @@ def test_c5_full_sweep_size11_visits_every_rank():
         assert cnt == 0
         full = ctx2.count(11)
         assert full.best_rank == hit.best_rank and full.count >= 1
+
+
+def test_shuffled_scan_on_block_beyond_2_32():
+    # RTid permutation i * 2246822507 mod block_total with block_total > 2^32
+    # (128-bit product): a window of local indices, device vs oracle
+    r = [r for r in load_golden("windows") if r["name"] == "C5dense_s13_op2"][0]
+    spec = spec_of(r["spec"])
+    t = O.OracleTable(4, 13)
+    off, cnt = t.operator_offset(13, 5), t.entry(13, 5)
+    assert cnt > 1 << 32
+    with DeviceContext(spec, 13) as ctx:
+        for a in (0, cnt // 3, cnt - 40000):
+            b = min(cnt, a + 40000)
+            want = O.scan_range(t, 4, spec.w, pairs_of(r["spec"]), 13, off, cnt, a, b, shuffled=True,
+                                threads=O.cpu_count())
+            got = ctx.scan_range(13, off, cnt, a, b, shuffled=True)
+            assert got == (want[0], want[2], want[3]), a

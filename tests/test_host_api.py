@@ -134,3 +134,15 @@ def test_gm_reciprocals_exact():
                 n = rng.randrange(1 << N_)
                 hi = (n * m) >> N_
                 assert (hi + ((n - hi) >> s1)) >> s2 == n // d
+
+
+def test_context_argument_errors_before_device():
+    # checks of simba_ctx_create that run before any device work
+    spec = S.Specification.of([((1,) * 10, 0)], k=10)
+    with pytest.raises(ValueError, match="2\\^64"):
+        S.DeviceContext(spec, 24)  # T[s][8] >= 2^64 for k=10 well below size 24
+    with pytest.raises(ValueError):
+        S.DeviceContext(S.Specification.of([((1,), 0)], k=1), 25)  # beyond SIMBA_MAX_SIZE
+    big_k = S.Specification.of([((0,) * 65, 0)], k=65)
+    with pytest.raises(ValueError):
+        S.DeviceContext(big_k, 3)
