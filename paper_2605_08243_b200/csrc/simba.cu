@@ -577,6 +577,155 @@ __device__ __noinline__ void sweep_b(const KParams &p, const Staged &st, const S
     }
 }
 
+// Variant T (transposed): for units whose rows are short (R2 < 1024) but
+// numerous.  Each lane holds the left values of 4 rows (loaded once,
+// coalesced), and a warp-uniform loop runs over d2: per d2 the right-fixed
+// P(., vR) segment, its merge into the outer chain and the folded test are
+// computed once for 128 candidates, so the per-candidate cost is one masked
+// LOP3 test (plus the remaining chain when the last segment cannot fold).
+template <class W>
+struct PCoefR {
+    W Am, Bm, Ax, Ca, Da, Cb, Sb;
+};
+
+template <class W>
+__device__ __forceinline__ PCoefR<W> pcoef_right(int pop)
+{
+    const W Z = (W)0, O = (W)~(W)0, ONE = (W)1;
+    switch (pop) {  // P(v, vR) with the right operand fixed
+    case OP_AND: return PCoefR<W>{O, Z, Z, Z, ONE, Z, ONE};
+    case OP_OR: return PCoefR<W>{O, O, O, Z, ONE, Z, ONE};
+    case OP_XOR: return PCoefR<W>{Z, O, O, Z, ONE, Z, ONE};
+    case OP_ADD: return PCoefR<W>{Z, O, Z, Z, ONE, O, ONE};
+    case OP_SUB: return PCoefR<W>{Z, O, Z, Z, ONE, O, O};  // v - vR: b = -vR
+    default: return PCoefR<W>{Z, O, Z, ONE, Z, Z, ONE};   // MUL
+    }
+}
+
+template <class W>
+__device__ __forceinline__ Seg<W> first_seg_r(const PCoefR<W> &k, W vR, const Seg<W> &s)
+{
+    const W gm = (vR & k.Am) ^ k.Bm, gx = vR & k.Ax, ga = vR * k.Ca + k.Da, gb = (vR & k.Cb) * k.Sb;
+    return Seg<W>{gm & s.m, (gx & s.m) ^ s.x, s.a * ga, s.a * gb + s.b};
+}
+
+template <class W, int E, int NT, bool X2D>
+__device__ __noinline__ void sweep_t(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
+                                     const PCoefR<W> &kcr, const Seg<W> &so0, const Seg<W> (&rest)[NT],
+                                     const Seg<W> (&sl)[MAXSL], W y0, XU xu, uint64_t ubase, uint32_t R2,
+                                     uint32_t off2, uint64_t row0, uint64_t nrows, int lane, uint64_t &my_count)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Tabs *t = stabs();
+    const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));
+    const W *g0 = reinterpret_cast<const W *>(p.gtbl);
+    const W mask = (W)p.mask;
+    const W y0m = y0 & mask;
+    Seg<W> c[NT], slr[MAXSL];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+        c[i] = rest[i];
+#pragma unroll
+    for (int i = 0; i < MAXSL; ++i)
+        slr[i] = sl[i];
+    const Seg<W> s0 = so0;
+    const PCoefR<W> k = kcr;
+    W tmF = mask, tcF = y0m;
+    bool foldF = false;
+    if constexpr (NT >= 2)
+        foldF = fold_last(c[NT - 1], y0m, mask, tmF, tcF);
+    // NT == 1: c[0].a = s0.a * (vR * Ca + Da) is constant unless P is MUL
+    const bool constc = k.Ca == (W)0;
+    W inv0 = (W)1;
+    bool inv0_ok = false;
+    if constexpr (NT == 1) {
+        if (constc) {
+            const W a0 = s0.a * k.Da;
+            inv0_ok = (a0 & (W)1) != 0;
+            if (inv0_ok)
+                inv0 = modinv_odd(a0);
+        }
+    }
+    const W *tr = t0 + off2;
+    for (uint64_t rb = 0; rb < nrows; rb += 128) {
+        W xv[4];
+        bool rv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint64_t r = rb + lane + 32 * i;
+            rv[i] = r < nrows;
+            W in = (W)0;
+            if (rv[i]) {
+                const uint64_t d1 = row0 + r;
+                if constexpr (X2D) {
+                    const uint64_t dy = div_T(t, xu.sz1, d1);
+                    in = apply_bin<W>(xu.pxop, __ldg(g0 + xu.offy + dy), __ldg(g0 + xu.off1 + (d1 - dy * xu.R1p)));
+                } else {
+                    in = __ldg(g0 + xu.off1 + d1);
+                }
+            }
+            xv[i] = segs_apply(slr, in);
+        }
+        for (uint32_t d2 = 0; d2 < R2; ++d2) {
+            c[0] = first_seg_r(k, tr[d2], s0);
+            bool h[4];
+            if constexpr (NT == 1) {
+                W tm, tc;
+                bool fold;
+                if (constc) {
+                    fold = inv0_ok;
+                    tm = c[0].m & mask;
+                    tc = (((y0m - c[0].b) * inv0) ^ c[0].x) & mask;
+                } else {
+                    fold = fold_last(c[0], y0m, mask, tm, tc);
+                }
+                if (fold) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        h[i] = rv[i] && ((xv[i] & tm) ^ tc) == 0;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        h[i] = rv[i] && ((seg_apply(c[0], xv[i]) & mask) ^ y0m) == 0;
+                }
+            } else {
+                if (foldF) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        h[i] = rv[i] && ((chain_k<W, NT - 1>(c, xv[i]) & tmF) ^ tcF) == 0;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        h[i] = rv[i] && ((chain_k<W, NT>(c, xv[i]) & mask) ^ y0m) == 0;
+                }
+            }
+            if (__any_sync(FULL, h[0] || h[1] || h[2] || h[3])) {
+                for (int i = 0; i < 4; ++i)
+                    on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h[i], row0 + rb + lane + 32 * i, d2,
+                                  my_count);
+            }
+        }
+    }
+}
+
+template <class W, int E, int NT>
+__device__ __forceinline__ void dispatch_t_nt(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
+                                              const PCoefR<W> &kcr, const Seg<W> &so0, const Seg<W> (&chain)[8],
+                                              const Seg<W> (&sl)[MAXSL], W y0, const XU &xu, uint64_t ubase,
+                                              uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, int lane,
+                                              uint64_t &cnt)
+{
+    Seg<W> rest[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+        rest[i] = chain[i];
+    if (xu.x2d)
+        sweep_t<W, E, NT, true>(p, st, sx, pop, kcr, so0, rest, sl, y0, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+    else
+        sweep_t<W, E, NT, false>(p, st, sx, pop, kcr, so0, rest, sl, y0, xu, ubase, R2, off2, row0, nrows, lane,
+                                 cnt);
+}
+
 __device__ __forceinline__ uint64_t read_best(const KParams &p)
 {
     unsigned long long b = 0;
@@ -736,56 +885,86 @@ __device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &s
                 }
             }
             const uint64_t u0 = n - ubase, u1 = stop - ubase;
-            if (R2 >= 32) {
-                if (ntA <= 1)
-                    dispatch_a_nt<W, E, 1>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
-                                           d2s, u1, lane, ss.count);
-                else if (ntA == 2)
-                    dispatch_a_nt<W, E, 2>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
-                                           d2s, u1, lane, ss.count);
-                else if (ntA == 3)
-                    dispatch_a_nt<W, E, 3>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
-                                           d2s, u1, lane, ss.count);
-                else
-                    dispatch_a_nt<W, E, 5>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, d1s,
-                                           d2s, u1, lane, ss.count);
-            } else {
-                // lane chain: LEFT, P(., vR), OUTER with vR = this lane's d2 value
-                const uint32_t lg = (uint32_t)lane / R2;
-                const uint32_t ld2 = (uint32_t)lane - lg * R2;
-                const W vR = t0[off2 + ld2];
-                SegChain<W, 8> ch;
-                ch.init();
-                if (pop != OP_NONE) {
-                    for (int i = 0; i < od.nsl; ++i)
-                        ch.then_seg(sl[i]);
-                    chain_right_fixed(ch, pop, vR);
+            // A / B sweep of the unit-local range [a, b)
+            auto sweep_ab = [&](uint64_t a, uint64_t b) {
+                const uint64_t ad1 = div_T(t, prsz, a);
+                const uint32_t ad2 = (uint32_t)(a - ad1 * R2);
+                if (R2 >= 32) {
+                    if (ntA <= 1)
+                        dispatch_a_nt<W, E, 1>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, ad1, ad2,
+                                               b, lane, ss.count);
+                    else if (ntA == 2)
+                        dispatch_a_nt<W, E, 2>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, ad1, ad2,
+                                               b, lane, ss.count);
+                    else if (ntA == 3)
+                        dispatch_a_nt<W, E, 3>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, ad1, ad2,
+                                               b, lane, ss.count);
+                    else
+                        dispatch_a_nt<W, E, 5>(p, st, sx, pop, kc, s0, chainA, sl, y0, xu, ubase, R2, off2, ad1, ad2,
+                                               b, lane, ss.count);
                 } else {
-                    ch.then_affine((W)0, vR);  // value = vR whatever the row input
+                    // lane chain: LEFT, P(., vR), OUTER with vR = this lane's d2 value
+                    const uint32_t lg = (uint32_t)lane / R2;
+                    const uint32_t ld2 = (uint32_t)lane - lg * R2;
+                    const W vR = t0[off2 + ld2];
+                    SegChain<W, 8> ch;
+                    ch.init();
+                    if (pop != OP_NONE) {
+                        for (int i = 0; i < od.nsl; ++i)
+                            ch.then_seg(sl[i]);
+                        chain_right_fixed(ch, pop, vR);
+                    } else {
+                        ch.then_affine((W)0, vR);  // value = vR whatever the row input
+                    }
+                    for (int i = 0; i < nso; ++i)
+                        ch.then_seg(so[i]);
+                    // fold this lane's last segment into the test when invertible
+                    const W mask = (W)p.mask;
+                    W tm = mask, tc = y0 & mask;
+                    int nl = ch.n;
+                    if (nl > 0 && fold_last(ch.last(), (W)(y0 & mask), mask, tm, tc)) {
+                        ch.set_last(seg_identity<W>());
+                        --nl;
+                    }
+                    const int nt = (int)__reduce_max_sync(FULL, (unsigned)nl);
+                    if (nt == 0)
+                        dispatch_b_nt<W, E, 1>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, ad1, a, b, lane,
+                                               ss.count);
+                    else if (nt <= 2)
+                        dispatch_b_nt<W, E, 2>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, ad1, a, b, lane,
+                                               ss.count);
+                    else if (nt <= 4)
+                        dispatch_b_nt<W, E, 4>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, ad1, a, b, lane,
+                                               ss.count);
+                    else
+                        dispatch_b_nt<W, E, 8>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, ad1, a, b, lane,
+                                               ss.count);
                 }
-                for (int i = 0; i < nso; ++i)
-                    ch.then_seg(so[i]);
-                // fold this lane's last segment into the test when invertible
-                const W mask = (W)p.mask;
-                W tm = mask, tc = y0 & mask;
-                int nl = ch.n;
-                if (nl > 0 && fold_last(ch.last(), (W)(y0 & mask), mask, tm, tc)) {
-                    ch.set_last(seg_identity<W>());
-                    --nl;
-                }
-                const int nt = (int)__reduce_max_sync(FULL, (unsigned)nl);
-                if (nt == 0)
-                    dispatch_b_nt<W, E, 1>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, d1s, u0, u1, lane,
-                                           ss.count);
-                else if (nt <= 2)
-                    dispatch_b_nt<W, E, 2>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, d1s, u0, u1, lane,
-                                           ss.count);
-                else if (nt <= 4)
-                    dispatch_b_nt<W, E, 4>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, d1s, u0, u1, lane,
-                                           ss.count);
+            };
+            // full rows of a short-row unit go to the transposed sweep
+            const uint64_t rfirst = (d2s == 0) ? d1s : d1s + 1;  // first complete row
+            const uint64_t rend = u1 / R2;                       // rows below it are complete
+            if (pop != OP_NONE && R2 < 1024 && rend >= rfirst + 64) {
+                if (rfirst * R2 > u0)
+                    sweep_ab(u0, rfirst * R2);
+                const PCoefR<W> kcr = pcoef_right<W>(pop);
+                const uint64_t nr = rend - rfirst;
+                if (ntA <= 1)
+                    dispatch_t_nt<W, E, 1>(p, st, sx, pop, kcr, s0, chainA, sl, y0, xu, ubase, R2, off2, rfirst, nr,
+                                           lane, ss.count);
+                else if (ntA == 2)
+                    dispatch_t_nt<W, E, 2>(p, st, sx, pop, kcr, s0, chainA, sl, y0, xu, ubase, R2, off2, rfirst, nr,
+                                           lane, ss.count);
+                else if (ntA == 3)
+                    dispatch_t_nt<W, E, 3>(p, st, sx, pop, kcr, s0, chainA, sl, y0, xu, ubase, R2, off2, rfirst, nr,
+                                           lane, ss.count);
                 else
-                    dispatch_b_nt<W, E, 8>(p, st, sx, pop, ch.s, tm, tc, xu, ubase, R2, off2, d1s, u0, u1, lane,
-                                           ss.count);
+                    dispatch_t_nt<W, E, 5>(p, st, sx, pop, kcr, s0, chainA, sl, y0, xu, ubase, R2, off2, rfirst, nr,
+                                           lane, ss.count);
+                if (u1 > rend * R2)
+                    sweep_ab(rend * R2, u1);
+            } else {
+                sweep_ab(u0, u1);
             }
         }
         n = stop;
