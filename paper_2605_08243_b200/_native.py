@@ -97,6 +97,7 @@ SIGNATURES = {
     "simba_ctx_info": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int)] * 7),
     "simba_ctx_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "simba_ctx_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "simba_ctx_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int]),
     "simba_int32_peak": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "simba_last_error": (C.c_char_p, []),
     "simba_device_count": (C.c_int, []),

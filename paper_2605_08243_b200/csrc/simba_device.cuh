@@ -16,6 +16,23 @@ constexpr int MAXSO = 4;  // outer-spine segments held in registers
 constexpr int MAXSL = 2;  // left-spine segments held in registers
 constexpr unsigned FULL = 0xffffffffu;
 
+// Path statistics for diagnostics builds (-DSIMBA_STATS): calls and
+// candidates per sweep path, read back with simba_ctx_stats.
+enum : int { ST_RF_FOLD = 0, ST_RF_GEN, ST_RF_ROW, ST_CF_FOLD, ST_CF_GEN, ST_T, ST_A, ST_B, ST_DIRECT, ST_N };
+#ifdef SIMBA_STATS
+#define SIMBA_STAT(p, i, cands)                                                         \
+    do {                                                                                \
+        if ((threadIdx.x & 31) == 0) {                                                  \
+            atomicAdd(&(p).stats[2 * (i)], 1ull);                                       \
+            atomicAdd(&(p).stats[2 * (i) + 1], (unsigned long long)(cands));            \
+        }                                                                               \
+    } while (0)
+#else
+#define SIMBA_STAT(p, i, cands) \
+    do {                        \
+    } while (0)
+#endif
+
 // Operator slots in the fixed enumeration order (expr.py:22-32).
 enum : int { OP_NOT = 0, OP_AND, OP_OR, OP_XOR, OP_NEG, OP_ADD, OP_SUB, OP_MUL, OP_NONE = 8 };
 
@@ -59,6 +76,7 @@ struct KParams {
     unsigned long long *visited;  // candidates evaluated
     unsigned long long *units;    // [0] units decoded, [1] units on the per-rank path
     unsigned int *flags;          // bit 0: stopped by the time budget
+    unsigned long long *stats;    // [2*path] calls, [2*path+1] candidates (SIMBA_STATS builds)
 };
 
 // ---------------------------------------------------------------------------
@@ -222,7 +240,7 @@ __device__ __noinline__ W eval_rpn(const int8_t *buf, int size, const TX *x)
 // ---------------------------------------------------------------------------
 
 template <class W>
-struct Seg {
+struct __align__(16) Seg {
     W m, x, a, b;
 };
 
@@ -323,113 +341,6 @@ struct SegList {
         }
     }
 };
-
-// Chain in application order (first segment applied first); `then` appends a
-// function applied after everything already in the chain, merging it into the
-// last segment when the composition stays a single LOP3+IMAD pair.
-template <class W, int CAP>
-struct SegChain {
-    Seg<W> s[CAP];
-    int n;
-    bool a_id;  // last segment's affine part is the identity (structurally)
-    bool ovf;
-    __device__ __forceinline__ void init()
-    {
-        n = 0;
-        a_id = true;
-        ovf = false;
-#pragma unroll
-        for (int i = 0; i < CAP; ++i)
-            s[i] = seg_identity<W>();
-    }
-    __device__ __forceinline__ void push(W m, W x, W a, W b, bool aid)
-    {
-        if (n >= CAP) {
-            ovf = true;
-            return;
-        }
-#pragma unroll
-        for (int i = 0; i < CAP; ++i)
-            if (i == n)
-                s[i] = Seg<W>{m, x, a, b};
-        ++n;
-        a_id = aid;
-    }
-    __device__ __forceinline__ Seg<W> last() const
-    {
-        Seg<W> r = seg_identity<W>();
-#pragma unroll
-        for (int i = 0; i < CAP; ++i)
-            if (i == n - 1)
-                r = s[i];
-        return r;
-    }
-    __device__ __forceinline__ void set_last(const Seg<W> &v)
-    {
-#pragma unroll
-        for (int i = 0; i < CAP; ++i)
-            if (i == n - 1)
-                s[i] = v;
-    }
-    // v -> (v & m) ^ x applied after the chain
-    __device__ __forceinline__ void then_bitwise(W m, W x)
-    {
-        if (n > 0 && a_id) {
-            Seg<W> c = last();  // A is identity: ((v&M)^X)&m ^ x
-            c.x = (c.x & m) ^ x;
-            c.m = c.m & m;
-            set_last(c);
-        } else {
-            push(m, x, (W)1, (W)0, true);
-        }
-    }
-    // v -> a*v + b applied after the chain: always merges
-    __device__ __forceinline__ void then_affine(W a, W b)
-    {
-        if (n > 0) {
-            Seg<W> c = last();
-            c.b = a * c.b + b;
-            c.a = a * c.a;
-            set_last(c);
-            a_id = false;
-        } else {
-            push((W)~(W)0, (W)0, a, b, false);
-        }
-    }
-    __device__ __forceinline__ void then_seg(const Seg<W> &g)
-    {
-        then_bitwise(g.m, g.x);
-        then_affine(g.a, g.b);
-    }
-};
-
-// fixed-operand form of P: left operand fixed (v = right value)
-template <class W, int CAP>
-__device__ __forceinline__ void chain_left_fixed(SegChain<W, CAP> &c, int op, W s)
-{
-    switch (op) {
-    case OP_AND: c.then_bitwise(s, (W)0); break;
-    case OP_OR: c.then_bitwise((W)~s, s); break;
-    case OP_XOR: c.then_bitwise((W)~(W)0, s); break;
-    case OP_ADD: c.then_affine((W)1, s); break;
-    case OP_SUB: c.then_affine((W)~(W)0, s); break;  // s - v
-    default: c.then_affine(s, (W)0); break;          // MUL
-    }
-}
-
-// fixed-operand form of P: right operand fixed (v = left value)
-template <class W, int CAP>
-__device__ __forceinline__ void chain_right_fixed(SegChain<W, CAP> &c, int op, W r)
-{
-    switch (op) {
-    case OP_AND: c.then_bitwise(r, (W)0); break;
-    case OP_OR: c.then_bitwise((W)~r, r); break;
-    case OP_XOR: c.then_bitwise((W)~(W)0, r); break;
-    case OP_ADD: c.then_affine((W)1, r); break;
-    case OP_SUB: c.then_affine((W)1, (W)0 - r); break;  // v - r
-    default: c.then_affine(r, (W)0); break;            // MUL
-    }
-}
 
 template <class W, int N>
 __device__ __forceinline__ W segs_apply(const Seg<W> (&s)[N], W v)
@@ -551,11 +462,21 @@ struct SegStash {
     Seg<W> sl[E][MAXSL];
 };
 
+// per-warp tile buffer: per-row (RF) or per-column (CF) test parameters
+constexpr int TILE_BUF = 128;
+static_assert(TILE_BUF % 32 == 0, "rows are produced 32 per step");
+
+template <class W>
+struct __align__(2 * sizeof(W)) TPair {
+    W m, c;
+};
+
 template <class W, int E>
 struct WarpLevels {
     LevelStack<W, E> outer;
     LevelStack<W, E> xs;
     SegStash<W, E> stash;
+    Seg<W> tbuf[TILE_BUF];  // per-row / per-column segments, or (m, c) pairs
 };
 
 template <class W, int E>

@@ -250,6 +250,17 @@ class DeviceContext:
         N.check_rc(N.lib.simba_ctx_stream(self._ptr, C.byref(h)))
         return h.value or 0
 
+    PATHS = ("rf_fold", "rf_gen", "rf_row", "cf_fold", "cf_gen", "t", "a", "b", "direct")
+
+    def path_stats(self) -> dict:
+        """Per-path (calls, candidates) of the unit kernel since creation;
+        empty unless libsimba was built with -DSIMBA_STATS (diagnostics)."""
+        buf = (C.c_uint64 * (2 * len(self.PATHS)))()
+        n = N.lib.simba_ctx_stats(self._ptr, buf, len(buf))
+        if n < 0:
+            N.check_rc(n)
+        return {name: (buf[2 * i], buf[2 * i + 1]) for i, name in enumerate(self.PATHS) if 2 * i + 1 < n}
+
     def decode(self, rank: int, size: int) -> tuple[int, ...]:
         buf = (C.c_int32 * N.MAX_SIZE)()
         N.check_rc(N.lib.simba_decode(self._ptr, rank, size, buf))

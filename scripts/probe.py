@@ -20,6 +20,10 @@ def run(label, spec, sizes, **kw):
         for s in sizes:
             r = ctx.count(s)  # warm
             r = ctx.count(s)
+            st = ctx.path_stats()
+            if st:
+                tot = sum(v[1] for v in st.values()) or 1
+                print("   paths:", {k: (v[0], round(100 * v[1] / tot, 2)) for k, v in st.items() if v[0]})
             print(f"{label:22s} s={s:2d} T={r.visited:.3e} {r.kernel_ms:9.3f} ms "
                   f"{r.visited / (r.kernel_ms * 1e-3):.3e} cand/s cnt={r.count} units={r.units} "
                   f"rank_units={r.rank_units} ctx={tc*1e3:.0f}ms {info}", flush=True)
