@@ -487,22 +487,36 @@ struct TileArgs {
     Seg<W> res[MAXSO];
 };
 
+// floor(n / T[sz]) for n < 2^32 and T[sz] < 2^32 (32-bit Granlund-Montgomery)
+__device__ __forceinline__ uint32_t div_T32(const Tabs *t, int sz, uint32_t n)
+{
+    const uint32_t hi = __umulhi(n, t->m32[sz]);
+    return (hi + ((n - hi) >> t->sh1[sz])) >> t->sh2[sz];
+}
+
 // Row values of X-unit rows d0 + lane + 32 j (j < NJ): LEFT( left input ),
-// example 0.  All loads are issued before any is used (rows past `cnt` repeat
-// the last row; callers mask them).
+// example 0.  Rows past `cnt` repeat the last row (callers mask them); all
+// loads are issued before any is used (skipping unneeded 32-row groups with
+// uniform branches measured slower: it serialises the loads).
 template <class W, int NJ>
 __device__ __forceinline__ void rows_left(const W *g0, const XU &xu, uint64_t d0, uint32_t cnt, int lane,
                                           const Seg<W> (&sl)[MAXSL], W (&x)[NJ])
 {
     W in[NJ];
     if (xu.x2d) {
+        // rows d0 + o, o < 256: dy = dy0 + (rem0 + o) / R1p (R1p = T[sz1] < 2^27)
+        const Tabs *t = stabs();
+        const uint64_t dy0 = div_T(t, xu.sz1, d0);
+        const uint32_t rem0 = (uint32_t)(d0 - dy0 * xu.R1p);
+        const W *gy = g0 + xu.offy + dy0;
+        const W *g1 = g0 + xu.off1;
         W a[NJ], b[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-            const uint64_t d1 = d0 + min((uint32_t)lane + 32u * j, cnt - 1);
-            const uint64_t dy = div_T(stabs(), xu.sz1, d1);
-            a[j] = __ldg(g0 + xu.offy + dy);
-            b[j] = __ldg(g0 + xu.off1 + (d1 - dy * xu.R1p));
+            const uint32_t r = rem0 + min((uint32_t)lane + 32u * j, cnt - 1);
+            const uint32_t q = div_T32(t, xu.sz1, r);
+            a[j] = __ldg(gy + q);
+            b[j] = __ldg(g1 + (r - q * (uint32_t)xu.R1p));
         }
         switch (xu.pxop) {
         case OP_AND:
@@ -598,6 +612,31 @@ __device__ __forceinline__ bool hit8x4<uint32_t>(const uint32_t (&v)[8], const u
 }
 #undef SIMBA_L0
 #undef SIMBA_L4
+
+// Slow-path hit masks: bit k*8 + j set when candidate (k, j) passes (fully
+// unrolled, so the value arrays stay in registers; the callers walk the set
+// bits one at a time, all lanes together because on_hits votes).
+template <class W>
+__device__ __forceinline__ uint32_t hitmask8x4(const W (&v)[8], const W (&m)[4], const W (&c)[4])
+{
+    uint32_t b = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            b |= (uint32_t)(((v[j] & m[k]) ^ c[k]) == 0) << (k * 8 + j);
+    return b;
+}
+
+template <class W>
+__device__ __forceinline__ uint32_t hitmask8(const W (&v)[8], W m, W c)
+{
+    uint32_t b = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        b |= (uint32_t)(((v[j] & m) ^ c) == 0) << j;
+    return b;
+}
 
 // four consecutive (m, c) pairs from the tile buffer (16-byte aligned)
 template <class W>
@@ -712,15 +751,13 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, const S
                     W m[4], c[4];
                     load4(pb + r, m, c);
                     if (__any_sync(FULL, hit8x4(s, m, c))) {
-#pragma unroll 1
-                        for (int k = 0; k < 4; ++k) {
-#pragma unroll 1
-                            for (int j = 0; j < 8; ++j) {
-                                const uint32_t d2 = c0 + lane + 32 * j;
-                                const bool h = r + k < nr && d2 < chi && ((s[j] & m[k]) ^ c[k]) == 0;
-                                on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r + k, d2,
-                                              my_count);
-                            }
+                        uint32_t bits = hitmask8x4(s, m, c);
+                        while (__any_sync(FULL, bits != 0)) {
+                            const int b = bits ? __ffs(bits) - 1 : 0;
+                            const uint32_t k = b >> 3, d2 = c0 + lane + 32 * (b & 7);
+                            const bool h = bits != 0 && r + k < nr && d2 < chi;
+                            bits &= bits - 1;
+                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r + k, d2, my_count);
                         }
                     }
                 }
@@ -737,10 +774,12 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, const S
                         v[j] = u;
                     }
                     if (__any_sync(FULL, hit8(v, TM, TC))) {
-#pragma unroll 1
-                        for (int j = 0; j < 8; ++j) {
-                            const uint32_t d2 = c0 + lane + 32 * j;
-                            const bool h = d2 < chi && ((v[j] & TM) ^ TC) == 0;
+                        uint32_t bits = hitmask8(v, TM, TC);
+                        while (__any_sync(FULL, bits != 0)) {
+                            const int b = bits ? __ffs(bits) - 1 : 0;
+                            const uint32_t d2 = c0 + lane + 32 * b;
+                            const bool h = bits != 0 && d2 < chi;
+                            bits &= bits - 1;
                             on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, d2, my_count);
                         }
                     }
@@ -806,14 +845,13 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, const S
                 W m[4], c[4];
                 load4(pb + cc, m, c);
                 if (__any_sync(FULL, hit8x4(x, m, c))) {
-#pragma unroll 1
-                    for (int k = 0; k < 4; ++k) {
-#pragma unroll 1
-                        for (int j = 0; j < 8; ++j) {
-                            const uint32_t r = lane + 32 * j;
-                            const bool h = r < nb && cc + k < R2 && ((x[j] & m[k]) ^ c[k]) == 0;
-                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc + k, my_count);
-                        }
+                    uint32_t bits = hitmask8x4(x, m, c);
+                    while (__any_sync(FULL, bits != 0)) {
+                        const int b = bits ? __ffs(bits) - 1 : 0;
+                        const uint32_t k = b >> 3, r = lane + 32 * (b & 7);
+                        const bool h = bits != 0 && r < nb && cc + k < R2;
+                        bits &= bits - 1;
+                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc + k, my_count);
                     }
                 }
             }
@@ -830,10 +868,12 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, const S
                     v[j] = u;
                 }
                 if (__any_sync(FULL, hit8(v, TM, TC))) {
-#pragma unroll 1
-                    for (int j = 0; j < 8; ++j) {
-                        const uint32_t r = lane + 32 * j;
-                        const bool h = r < nb && ((v[j] & TM) ^ TC) == 0;
+                    uint32_t bits = hitmask8(v, TM, TC);
+                    while (__any_sync(FULL, bits != 0)) {
+                        const int b = bits ? __ffs(bits) - 1 : 0;
+                        const uint32_t r = lane + 32 * b;
+                        const bool h = bits != 0 && r < nb;
+                        bits &= bits - 1;
                         on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc, my_count);
                     }
                 }
