@@ -170,7 +170,8 @@ int simba_int32_peak(int device, int iters, double *ops_per_s, double *kernel_ms
 
 /* Diagnostics: per-path (calls, candidates) counters of the unit kernel since
  * the context was created, in path order RF-fold, RF-gen, RF-row, CF-fold,
- * CF-gen, T, A, B, direct.  Copies up to n words and returns how many were
+ * CF-gen, then (calls, SM cycles) of outer odometer steps, X odometer steps
+ * and tile calls, then the per-rank (direct) path.  Copies up to n words and returns how many were
  * written; 0 unless the library was built with -DSIMBA_STATS. */
 int simba_ctx_stats(simba_ctx *ctx, uint64_t *out, int n);
 

@@ -478,14 +478,6 @@ __device__ __forceinline__ bool hit8<uint32_t>(const uint32_t (&v)[8], uint32_t 
     return r != 0;
 }
 
-// Per-P-block tile description: the folded outer test and the residual chain.
-template <class W>
-struct TileArgs {
-    W tm, tc;
-    int nres;
-    bool fold;  // P folds too: one LOP3 per candidate
-    Seg<W> res[MAXSO];
-};
 
 // floor(n / T[sz]) for n < 2^32 and T[sz] < 2^32 (32-bit Granlund-Montgomery)
 __device__ __forceinline__ uint32_t div_T32(const Tabs *t, int sz, uint32_t n)
@@ -899,6 +891,7 @@ __device__ __forceinline__ void dispatch_rf(const KParams &p, const Staged &st, 
                                             uint64_t &cnt)
 {
     SIMBA_STAT(p, nrows == 1 ? ST_RF_ROW : ta.fold ? ST_RF_FOLD : ST_RF_GEN, nrows * (chi - clo));
+    SIMBA_CYC_BEGIN(ct);
     const int nt = ta.fold ? 0 : gen_nt(pop, ta);
     if (nt == 0)
         tile_rf<W, E, 0>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, clo, chi, buf, lane, cnt);
@@ -910,6 +903,7 @@ __device__ __forceinline__ void dispatch_rf(const KParams &p, const Staged &st, 
         tile_rf<W, E, 3>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, clo, chi, buf, lane, cnt);
     else
         tile_rf<W, E, 5>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, clo, chi, buf, lane, cnt);
+    SIMBA_CYC_END(p, ST_CYC_TILE, ct);
 }
 
 template <class W, int E>
@@ -919,6 +913,7 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
                                             uint64_t nrows, Seg<W> *buf, int lane, uint64_t &cnt)
 {
     SIMBA_STAT(p, ta.fold ? ST_CF_FOLD : ST_CF_GEN, nrows * R2);
+    SIMBA_CYC_BEGIN(ct);
     const int nt = ta.fold ? 0 : gen_nt(pop, ta);
     if (nt == 0)
         tile_cf<W, E, 0>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, buf, lane, cnt);
@@ -930,6 +925,7 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
         tile_cf<W, E, 3>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, buf, lane, cnt);
     else
         tile_cf<W, E, 5>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, buf, lane, cnt);
+    SIMBA_CYC_END(p, ST_CYC_TILE, ct);
 }
 
 // All ranks [n, n1) of one P block (n1 <= pend).  The outer chain and P's
@@ -964,14 +960,24 @@ __device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &s
     const uint32_t R2 = (uint32_t)t->T[prsz], off2 = t->toff[prsz];
     const uint64_t pb = od.pb;
     const bool early = (p.mode == SIMBA_MODE_SEARCH);
-    // tile description of this P block: folded outer test + residual chain
-    TileArgs<W> ta;
-    {
+    // tile description of this P block: folded outer test + residual chain,
+    // cached per outer chain (sibling P blocks share it)
+    if (od.L->tac_gen != od.gen) {
+        TileArgs<W> f;
         const W mask = (W)p.mask;
-        ta.nres = fold_outer(so, nso, (W)(y0 & mask), mask, ta.tm, ta.tc);
+        f.nres = fold_outer(so, nso, (W)(y0 & mask), mask, f.tm, f.tc);
 #pragma unroll
         for (int i = 0; i < MAXSO; ++i)
-            ta.res[i] = (i < ta.nres) ? so[i] : seg_identity<W>();
+            f.res[i] = (i < f.nres) ? so[i] : seg_identity<W>();
+        __syncwarp();
+        if (lane == 0) {
+            od.L->tac = f;
+            od.L->tac_gen = od.gen;
+        }
+        __syncwarp();
+    }
+    TileArgs<W> ta = od.L->tac;
+    {
         const bool pbw = (pop == OP_AND || pop == OP_OR || pop == OP_XOR || pop == OP_NONE);
         ta.fold = ta.nres == 0 && (pbw || is_low(ta.tm));
     }
@@ -987,7 +993,9 @@ __device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &s
         } else {
             const uint64_t q = div_T(t, prsz, n - pb);
             if (!od.have_x || q >= od.qend) {
+                SIMBA_CYC_BEGIN(cx);
                 od.decode_x(q);
+                SIMBA_CYC_END(p, ST_CYC_X, cx);
                 if constexpr (E > 1) {
                     if (lane < E) {
 #pragma unroll
@@ -1156,6 +1164,10 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     const int lane = threadIdx.x & 31;
     Odometer<W, E> od;
     od.L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
+    od.gen = 0;
+    if (lane == 0)
+        od.L->tac_gen = ~0u;
+    __syncwarp();
     od.gt_e = reinterpret_cast<const W *>(p.gtbl) + (size_t)(lane & (E - 1)) * p.gtbl_len;
     od.R0 = p.R0;
     od.RG = p.RG;
@@ -1185,7 +1197,9 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             od.reset();
             uint64_t n = c0;
             while (n < c1) {
+                SIMBA_CYC_BEGIN(co);
                 od.outer_at(n);
+                SIMBA_CYC_END(p, ST_CYC_OUTER, co);
                 const uint64_t pstop = min(od.pend, c1);
                 if (od.ovf_o) {
                     ++ss.units;

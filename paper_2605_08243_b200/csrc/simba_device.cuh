@@ -18,7 +18,11 @@ constexpr unsigned FULL = 0xffffffffu;
 
 // Path statistics for diagnostics builds (-DSIMBA_STATS): calls and
 // candidates per sweep path, read back with simba_ctx_stats.
-enum : int { ST_RF_FOLD = 0, ST_RF_GEN, ST_RF_ROW, ST_CF_FOLD, ST_CF_GEN, ST_T, ST_A, ST_B, ST_DIRECT, ST_N };
+enum : int {
+    ST_RF_FOLD = 0, ST_RF_GEN, ST_RF_ROW, ST_CF_FOLD, ST_CF_GEN,
+    ST_CYC_OUTER, ST_CYC_X, ST_CYC_TILE,  // (calls, SM cycles) of the odometer steps and tile calls
+    ST_DIRECT, ST_N
+};
 #ifdef SIMBA_STATS
 #define SIMBA_STAT(p, i, cands)                                                         \
     do {                                                                                \
@@ -27,9 +31,17 @@ enum : int { ST_RF_FOLD = 0, ST_RF_GEN, ST_RF_ROW, ST_CF_FOLD, ST_CF_GEN, ST_T, 
             atomicAdd(&(p).stats[2 * (i) + 1], (unsigned long long)(cands));            \
         }                                                                               \
     } while (0)
+#define SIMBA_CYC_BEGIN(v) const long long v = clock64()
+#define SIMBA_CYC_END(p, i, v) SIMBA_STAT(p, i, clock64() - (v))
 #else
 #define SIMBA_STAT(p, i, cands) \
     do {                        \
+    } while (0)
+#define SIMBA_CYC_BEGIN(v) \
+    do {                   \
+    } while (0)
+#define SIMBA_CYC_END(p, i, v) \
+    do {                       \
     } while (0)
 #endif
 
@@ -471,12 +483,24 @@ struct __align__(2 * sizeof(W)) TPair {
     W m, c;
 };
 
+// Per-P-block tile description: the outer chain folded into a masked
+// compare ((v & tm) ^ tc) == 0 plus the residual (unfolded) inner segments.
+template <class W>
+struct TileArgs {
+    W tm, tc;
+    int nres;
+    bool fold;  // P folds too: one LOP3 per candidate
+    Seg<W> res[MAXSO];
+};
+
 template <class W, int E>
 struct WarpLevels {
     LevelStack<W, E> outer;
     LevelStack<W, E> xs;
     SegStash<W, E> stash;
     Seg<W> tbuf[TILE_BUF];  // per-row / per-column segments, or (m, c) pairs
+    TileArgs<W> tac;        // folded outer chain of odometer generation tac_gen
+    uint32_t tac_gen;
 };
 
 template <class W, int E>
@@ -499,6 +523,7 @@ struct Odometer {
     Seg<W> so[MAXSO], sl[MAXSL];
     int nso, nsl;
     bool so0_bw;           // innermost outer segment has a bitwise part
+    uint32_t gen;          // bumped whenever the outer chain (so) is recomposed
     bool ovf_o, ovf_l;
 
     __device__ __forceinline__ void reset()
@@ -555,9 +580,12 @@ struct Odometer {
     {
         const Tabs *t = stabs();
         LevelStack<W, E> &st = L->outer;
+        bool changed = !have_outer;
         if (have_outer) {
-            while (no > 0 && n >= st.end[no - 1])
+            while (no > 0 && n >= st.end[no - 1]) {
                 --no;
+                changed = true;
+            }
         } else {
             no = 0;
         }
@@ -570,6 +598,7 @@ struct Odometer {
             if (op == OP_NOT || op == OP_NEG) {
                 // child region = the whole operator block: [n - r, n - r + T[sz-1])
                 push_level(st, no++, op, sz - 1, n - r + t->T[sz - 1], (W)0);
+                changed = true;
                 --sz;
                 continue;
             }
@@ -587,6 +616,7 @@ struct Odometer {
             }
             const W sv = sib_value(j, q);
             push_level(st, no++, op, rsz, n - rr + t->T[rsz], sv);
+            changed = true;
             sz = rsz;
             r = rr;
         }
@@ -596,7 +626,10 @@ struct Odometer {
             pend = pb + t->T[sz];
         }
         __syncwarp();
-        compose<MAXSO>(st, no, so, nso, ovf_o, so0_bw);
+        if (changed) {  // sibling P blocks keep the outer chain
+            compose<MAXSO>(st, no, so, nso, ovf_o, so0_bw);
+            ++gen;
+        }
         have_outer = true;
         have_x = false;
         nx = 0;

@@ -250,7 +250,7 @@ class DeviceContext:
         N.check_rc(N.lib.simba_ctx_stream(self._ptr, C.byref(h)))
         return h.value or 0
 
-    PATHS = ("rf_fold", "rf_gen", "rf_row", "cf_fold", "cf_gen", "t", "a", "b", "direct")
+    PATHS = ("rf_fold", "rf_gen", "rf_row", "cf_fold", "cf_gen", "cyc_outer", "cyc_x", "cyc_tile", "direct")
 
     def path_stats(self) -> dict:
         """Per-path (calls, candidates) of the unit kernel since creation;

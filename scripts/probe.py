@@ -22,8 +22,13 @@ def run(label, spec, sizes, **kw):
             r = ctx.count(s)
             st = ctx.path_stats()
             if st:
-                tot = sum(v[1] for v in st.values()) or 1
-                print("   paths:", {k: (v[0], round(100 * v[1] / tot, 2)) for k, v in st.items() if v[0]})
+                cyc = {k: v for k, v in st.items() if k.startswith("cyc")}
+                paths = {k: v for k, v in st.items() if not k.startswith("cyc")}
+                tot = sum(v[1] for v in paths.values()) or 1
+                print("   paths:", {k: (v[0], round(100 * v[1] / tot, 2)) for k, v in paths.items() if v[0]})
+                warps = info["grid_blocks"] * info["block_threads"] // 32
+                print("   cycles per warp:", {k: (v[0], round(v[1] / warps / 1e6, 2)) for k, v in cyc.items()},
+                      "Mcyc; kernel", round(r.kernel_ms * 1.965e3 / 1e3, 2), "Mcyc at 1965 MHz")
             print(f"{label:22s} s={s:2d} T={r.visited:.3e} {r.kernel_ms:9.3f} ms "
                   f"{r.visited / (r.kernel_ms * 1e-3):.3e} cand/s cnt={r.count} units={r.units} "
                   f"rank_units={r.rank_units} ctx={tc*1e3:.0f}ms {info}", flush=True)
