@@ -1,6 +1,6 @@
 """Summarise an ncu --set full report into profiles/<name>.json (run here, no GPU).
 
-usage: python scripts/ncu_summary.py gpurun_out/prof.ncu-rep profiles/name.json [label]
+usage: python scripts/ncu_summary.py gpurun_out/prof.ncu-rep profiles/name.json [label] [candidates/launch]
 """
 import csv
 import io
@@ -15,7 +15,7 @@ def page(rep, *args):
     return list(csv.reader(io.StringIO(out)))
 
 
-def main(rep, dst, label=""):
+def main(rep, dst, label="", candidates=None):
     raw = page(rep, "--page", "raw")
     h, units, vals = raw[0], raw[1], raw[2]
     d = dict(zip(h, vals))
@@ -56,6 +56,7 @@ def main(rep, dst, label=""):
     top = sorted(rows, key=lambda r: -f(r[ie]))[:24]
     summary = {
         "label": label, "report": rep, "metrics": metrics,
+        "candidates_per_launch": int(candidates) if candidates else None,
         "dram_bytes_per_launch": (bytes_("dram__bytes_read.sum") or 0) + (bytes_("dram__bytes_write.sum") or 0),
         "stall_share": {k: round(v / tot, 4) for k, v in sorted(agg.items(), key=lambda x: -x[1]) if v},
         "top_sass_by_executions": [{"sass": r[isrc], "executed": int(f(r[ie]))} for r in top],
