@@ -679,12 +679,17 @@ __device__ __forceinline__ Seg<W> gen_seg(Seg<W> g, bool merge, const Seg<W> &r0
 // per-row (m, c), four rows per step; NT >= 1: per-row segment (merged P)
 // followed by res[1 or 0 ..], NT segments in all, then the (TM, TC) test.
 template <class W, int E, int NT>
-__device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
-                                     const TileArgs<W> &ta, const Seg<W> (&sl)[MAXSL], XU xu, uint64_t ubase,
+__device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop, XU xu, uint64_t ubase,
                                      uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, uint32_t clo,
-                                     uint32_t chi, Seg<W> *buf, int lane, uint64_t &my_count)
+                                     uint32_t chi, int lane, uint64_t &my_count)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    // this warp's shared block: folded outer chain, LEFT segments, tile buffer
+    WarpLevels<W, E> *L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
+    const SegStash<W, E> *sx = &L->stash;
+    Seg<W> *buf = L->tbuf;
+    const TileArgs<W> &ta = L->tac;
+    const Seg<W> (&sl)[MAXSL] = L->sl0;
     const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);
     TPair<W> *pb = reinterpret_cast<TPair<W> *>(buf);
@@ -786,12 +791,16 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, const S
 // hold 8 row values, columns are warp-uniform: per-column (m, c) (folded,
 // four columns per step) or per-column segments (GEN) in the buffer.
 template <class W, int E, int NT>
-__device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
-                                     const TileArgs<W> &ta, const Seg<W> (&sl)[MAXSL], XU xu, uint64_t ubase,
-                                     uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, Seg<W> *buf,
-                                     int lane, uint64_t &my_count)
+__device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop, XU xu, uint64_t ubase,
+                                     uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, int lane, uint64_t &my_count)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    // this warp's shared block: folded outer chain, LEFT segments, tile buffer
+    WarpLevels<W, E> *L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
+    const SegStash<W, E> *sx = &L->stash;
+    Seg<W> *buf = L->tbuf;
+    const TileArgs<W> &ta = L->tac;
+    const Seg<W> (&sl)[MAXSL] = L->sl0;
     const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);
     TPair<W> *pb = reinterpret_cast<TPair<W> *>(buf);
@@ -884,47 +893,42 @@ __device__ __forceinline__ int gen_nt(int pop, const TileArgs<W> &ta)
 }
 
 template <class W, int E>
-__device__ __forceinline__ void dispatch_rf(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
-                                            const TileArgs<W> &ta, const Seg<W> (&sl)[MAXSL], const XU &xu,
+__device__ __forceinline__ void dispatch_rf(const KParams &p, const Staged &st, int pop, int nt, const XU &xu,
                                             uint64_t ubase, uint32_t R2, uint32_t off2, uint64_t row0,
-                                            uint64_t nrows, uint32_t clo, uint32_t chi, Seg<W> *buf, int lane,
-                                            uint64_t &cnt)
+                                            uint64_t nrows, uint32_t clo, uint32_t chi, int lane, uint64_t &cnt)
 {
-    SIMBA_STAT(p, nrows == 1 ? ST_RF_ROW : ta.fold ? ST_RF_FOLD : ST_RF_GEN, nrows * (chi - clo));
+    SIMBA_STAT(p, nrows == 1 ? ST_RF_ROW : nt == 0 ? ST_RF_FOLD : ST_RF_GEN, nrows * (chi - clo));
     SIMBA_CYC_BEGIN(ct);
-    const int nt = ta.fold ? 0 : gen_nt(pop, ta);
     if (nt == 0)
-        tile_rf<W, E, 0>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, clo, chi, buf, lane, cnt);
+        tile_rf<W, E, 0>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     else if (nt == 1)
-        tile_rf<W, E, 1>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, clo, chi, buf, lane, cnt);
+        tile_rf<W, E, 1>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     else if (nt == 2)
-        tile_rf<W, E, 2>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, clo, chi, buf, lane, cnt);
+        tile_rf<W, E, 2>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     else if (nt == 3)
-        tile_rf<W, E, 3>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, clo, chi, buf, lane, cnt);
+        tile_rf<W, E, 3>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     else
-        tile_rf<W, E, 5>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, clo, chi, buf, lane, cnt);
+        tile_rf<W, E, 5>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     SIMBA_CYC_END(p, ST_CYC_TILE, ct);
 }
 
 template <class W, int E>
-__device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop,
-                                            const TileArgs<W> &ta, const Seg<W> (&sl)[MAXSL], const XU &xu,
+__device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, int pop, int nt, const XU &xu,
                                             uint64_t ubase, uint32_t R2, uint32_t off2, uint64_t row0,
-                                            uint64_t nrows, Seg<W> *buf, int lane, uint64_t &cnt)
+                                            uint64_t nrows, int lane, uint64_t &cnt)
 {
-    SIMBA_STAT(p, ta.fold ? ST_CF_FOLD : ST_CF_GEN, nrows * R2);
+    SIMBA_STAT(p, nt == 0 ? ST_CF_FOLD : ST_CF_GEN, nrows * R2);
     SIMBA_CYC_BEGIN(ct);
-    const int nt = ta.fold ? 0 : gen_nt(pop, ta);
     if (nt == 0)
-        tile_cf<W, E, 0>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, buf, lane, cnt);
+        tile_cf<W, E, 0>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
     else if (nt == 1)
-        tile_cf<W, E, 1>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, buf, lane, cnt);
+        tile_cf<W, E, 1>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
     else if (nt == 2)
-        tile_cf<W, E, 2>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, buf, lane, cnt);
+        tile_cf<W, E, 2>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
     else if (nt == 3)
-        tile_cf<W, E, 3>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, buf, lane, cnt);
+        tile_cf<W, E, 3>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
     else
-        tile_cf<W, E, 5>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, row0, nrows, buf, lane, cnt);
+        tile_cf<W, E, 5>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
     SIMBA_CYC_END(p, ST_CYC_TILE, ct);
 }
 
@@ -948,7 +952,7 @@ __device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &s
     }
     const Tabs *t = stabs();
     const W y0 = reinterpret_cast<const W *>(st.ys)[0];
-    Seg<W> so[MAXSO], sl[MAXSL];
+    Seg<W> so[MAXSO];
     if constexpr (E == 1) {
 #pragma unroll
         for (int i = 0; i < MAXSO; ++i)
@@ -976,12 +980,13 @@ __device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &s
         }
         __syncwarp();
     }
-    TileArgs<W> ta = od.L->tac;
+    // segments per candidate: 0 = folded (one LOP3), else the GEN chain length
+    int nt;
     {
+        const TileArgs<W> &tac = od.L->tac;
         const bool pbw = (pop == OP_AND || pop == OP_OR || pop == OP_XOR || pop == OP_NONE);
-        ta.fold = ta.nres == 0 && (pbw || is_low(ta.tm));
+        nt = (tac.nres == 0 && (pbw || is_low(tac.tm))) ? 0 : gen_nt(pop, tac);
     }
-    Seg<W> *tbuf = od.L->tbuf;
     while (n < n1) {
         uint64_t ubase, stop;
         XU xu{0, 0, 0, 0, 0, 0, 1};
@@ -996,6 +1001,12 @@ __device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &s
                 SIMBA_CYC_BEGIN(cx);
                 od.decode_x(q);
                 SIMBA_CYC_END(p, ST_CYC_X, cx);
+                if (lane == 0) {  // example 0's LEFT chain for the tiles
+#pragma unroll
+                    for (int i = 0; i < MAXSL; ++i)
+                        od.L->sl0[i] = od.sl[i];
+                }
+                __syncwarp();
                 if constexpr (E > 1) {
                     if (lane < E) {
 #pragma unroll
@@ -1023,15 +1034,6 @@ __device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &s
             SIMBA_STAT(p, ST_DIRECT, stop - n);
             direct_range<W>(p, st, n, stop, false, ss.count);
         } else {
-            if (pop != OP_NONE) {
-                if constexpr (E == 1) {
-#pragma unroll
-                    for (int i = 0; i < MAXSL; ++i)
-                        sl[i] = od.sl[i];
-                } else {
-                    bcast_seg_array<W, MAXSL>(od.sl, 0, sl);
-                }
-            }
             // unit-local candidates u = d1 * R2 + d2 in [u0, u1): full rows in
             // one RF (R2 >= kRFMin) or CF tile, partial rows as one-row RF tiles
             const uint64_t u1 = stop - ubase;
@@ -1042,16 +1044,14 @@ __device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &s
                 const uint32_t clo = (uint32_t)(u - rs);
                 if (clo != 0 || u1 - rs < R2) {
                     const uint32_t chi = (uint32_t)min((uint64_t)R2, u1 - rs);
-                    dispatch_rf<W, E>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, d1, 1, clo, chi, tbuf, lane,
-                                      ss.count);
+                    dispatch_rf<W, E>(p, st, pop, nt, xu, ubase, R2, off2, d1, 1, clo, chi, lane, ss.count);
                     u = rs + chi;
                 } else {
                     const uint64_t nf = div_T(t, prsz, u1 - u);
                     if (pop == OP_NONE || R2 >= kRFMin)
-                        dispatch_rf<W, E>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, d1, nf, 0, R2, tbuf, lane,
-                                          ss.count);
+                        dispatch_rf<W, E>(p, st, pop, nt, xu, ubase, R2, off2, d1, nf, 0, R2, lane, ss.count);
                     else
-                        dispatch_cf<W, E>(p, st, sx, pop, ta, sl, xu, ubase, R2, off2, d1, nf, tbuf, lane, ss.count);
+                        dispatch_cf<W, E>(p, st, pop, nt, xu, ubase, R2, off2, d1, nf, lane, ss.count);
                     u += nf * R2;
                 }
             }

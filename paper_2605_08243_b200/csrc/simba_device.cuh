@@ -500,6 +500,7 @@ struct WarpLevels {
     SegStash<W, E> stash;
     Seg<W> tbuf[TILE_BUF];  // per-row / per-column segments, or (m, c) pairs
     TileArgs<W> tac;        // folded outer chain of odometer generation tac_gen
+    Seg<W> sl0[MAXSL];      // example 0's LEFT chain of the current X unit
     uint32_t tac_gen;
 };
 
