@@ -30,6 +30,10 @@
 
 #include "simba_device.cuh"
 
+#ifndef SIMBA_UNIT_THREADS
+#define SIMBA_UNIT_THREADS 512
+#endif
+
 using namespace simba;
 typedef unsigned __int128 u128;
 
@@ -932,24 +936,137 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
     SIMBA_CYC_END(p, ST_CYC_TILE, ct);
 }
 
+// ---------------------------------------------------------------------------
+// plan / execute phases
+// ---------------------------------------------------------------------------
+//
+// unit_kernel alternates CTA-wide between a planning phase, in which every warp
+// advances its odometer and writes up to kDescPerWarp tile descriptors into the
+// CTA's queue (global, L2-resident), and an execution phase, in which all warps
+// drain the queue sorted by tile variant.  Each phase runs one small code
+// region on every warp of the SM, instead of every warp alternating between
+// the odometer and the tiles (instruction-cache refills and register reloads
+// at every transition cost ~30% of the time).
+
+constexpr int kDescPerWarp = 24;
+constexpr uint64_t kDescCands = 1u << 16;  // candidates per descriptor (load balance)
+constexpr int kVariants = 8;
+
+struct PlanShared {
+    unsigned int qn, qnext, active;
+    unsigned int start[kVariants];
+    uint8_t var[SIMBA_UNIT_THREADS / 32 * kDescPerWarp];
+    uint16_t order[SIMBA_UNIT_THREADS / 32 * kDescPerWarp];
+};
+
+__device__ __forceinline__ PlanShared *plan_shared(const KParams &p)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    return reinterpret_cast<PlanShared *>(smem + p.ps_off);
+}
+
+template <class W, int E>
+__device__ __forceinline__ TileDesc<W, E> *desc_queue(const KParams &p)
+{
+    return reinterpret_cast<TileDesc<W, E> *>(p.queue) + (size_t)blockIdx.x * p.qcap;
+}
+
+__device__ __forceinline__ int variant_of(int kind, int nt)
+{
+    return kind * 4 + (nt == 0 ? 0 : nt == 1 ? 1 : nt == 2 ? 2 : 3);
+}
+
+template <class W, int E>
+__device__ __forceinline__ void emit_tile(const KParams &p, const Odometer<W, E> &od, int kind, int pop, int nt,
+                                          const XU &xu, uint64_t ubase, uint32_t R2, uint32_t off2, uint64_t row0,
+                                          uint64_t nrows, uint32_t clo, uint32_t chi, int lane, int &emitted)
+{
+    PlanShared *ps = plan_shared(p);
+    unsigned int slot = 0;
+    if (lane == 0)
+        slot = atomicAdd(&ps->qn, 1u);
+    slot = __shfl_sync(FULL, slot, 0);
+    TileDesc<W, E> *d = desc_queue<W, E>(p) + slot;
+    if (lane == 0) {
+        d->ta = od.L->tac;
+#pragma unroll
+        for (int i = 0; i < MAXSL; ++i)
+            d->sl[i] = od.sl[i];  // lane 0 holds example 0's chain
+        d->ubase = ubase;
+        d->row0 = row0;
+        d->nrows = nrows;
+        d->R1p = xu.R1p;
+        d->R2 = R2;
+        d->off2 = off2;
+        d->clo = clo;
+        d->chi = chi;
+        d->off1 = xu.off1;
+        d->offy = xu.offy;
+        d->pop = (int8_t)pop;
+        d->kind = (int8_t)kind;
+        d->nt = (int8_t)nt;
+        d->aff = 0;
+        d->x2d = (int8_t)xu.x2d;
+        d->pxop = (int8_t)xu.pxop;
+        d->sz1 = (int8_t)xu.sz1;
+        d->szy = (int8_t)xu.szy;
+        ps->var[slot] = (uint8_t)variant_of(kind, nt);
+    }
+    if constexpr (E > 1) {  // lane e holds example e's chains (hit refinement)
+        if (lane < E) {
+#pragma unroll
+            for (int i = 0; i < MAXSO; ++i)
+                d->st.s.so[lane][i] = od.so[i];
+#pragma unroll
+            for (int i = 0; i < MAXSL; ++i)
+                d->st.s.sl[lane][i] = od.sl[i];
+        }
+    }
+    ++emitted;
+}
+
+// One descriptor: stage its chains in the warp's shared block, run the tile.
+template <class W, int E>
+__device__ __noinline__ void exec_desc(const KParams &p, const Staged &st, const TileDesc<W, E> *d, int lane,
+                                       uint64_t &cnt)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    WarpLevels<W, E> *L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
+    if (lane == 0) {
+        L->tac = d->ta;
+#pragma unroll
+        for (int i = 0; i < MAXSL; ++i)
+            L->sl0[i] = d->sl[i];
+    }
+    if constexpr (E > 1) {
+        if (lane < E) {
+#pragma unroll
+            for (int i = 0; i < MAXSO; ++i)
+                L->stash.so[lane][i] = d->st.s.so[lane][i];
+#pragma unroll
+            for (int i = 0; i < MAXSL; ++i)
+                L->stash.sl[lane][i] = d->st.s.sl[lane][i];
+        }
+    }
+    __syncwarp();
+    const XU xu{d->x2d, d->pxop, d->szy, d->sz1, d->offy, d->off1, d->R1p};
+    if (d->kind == 0)
+        dispatch_rf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, d->clo, d->chi,
+                          lane, cnt);
+    else
+        dispatch_cf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, lane, cnt);
+    __syncwarp();
+}
+
 // All ranks [n, n1) of one P block (n1 <= pend).  The outer chain and P's
 // operator are fixed for the whole block; the X odometer advances unit by
 // unit here, so consecutive units cost one decode_x step (usually a single
 // level).  Returns the first rank not scanned (n1 unless a search hit allows
 // early exit).
 template <class W, int E>
-__device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &st, Odometer<W, E> &od, uint64_t n,
-                                               uint64_t n1, int lane, SweepStats &ss)
+__device__ __forceinline__ uint64_t plan_pblock(const KParams &p, const Staged &st, Odometer<W, E> &od, uint64_t n,
+                                                uint64_t n1, int lane, SweepStats &ss, int &emitted, int cap)
 {
-    SegStash<W, E> *sx = &od.L->stash;
-    if constexpr (E > 1) {
-        if (lane < E) {
-#pragma unroll
-            for (int i = 0; i < MAXSO; ++i)
-                sx->so[lane][i] = od.so[i];
-        }
-        __syncwarp();
-    }
     const Tabs *t = stabs();
     const W y0 = reinterpret_cast<const W *>(st.ys)[0];
     Seg<W> so[MAXSO];
@@ -1001,20 +1118,6 @@ __device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &s
                 SIMBA_CYC_BEGIN(cx);
                 od.decode_x(q);
                 SIMBA_CYC_END(p, ST_CYC_X, cx);
-                if (lane == 0) {  // example 0's LEFT chain for the tiles
-#pragma unroll
-                    for (int i = 0; i < MAXSL; ++i)
-                        od.L->sl0[i] = od.sl[i];
-                }
-                __syncwarp();
-                if constexpr (E > 1) {
-                    if (lane < E) {
-#pragma unroll
-                        for (int i = 0; i < MAXSL; ++i)
-                            sx->sl[lane][i] = od.sl[i];
-                    }
-                    __syncwarp();
-                }
             }
             xu.x2d = od.x2d ? 1 : 0;
             xu.sz1 = od.sz1;
@@ -1035,23 +1138,25 @@ __device__ __forceinline__ uint64_t run_pblock(const KParams &p, const Staged &s
             direct_range<W>(p, st, n, stop, false, ss.count);
         } else {
             // unit-local candidates u = d1 * R2 + d2 in [u0, u1): full rows in
-            // one RF (R2 >= kRFMin) or CF tile, partial rows as one-row RF tiles
+            // RF (R2 >= kRFMin) or CF tiles of at most kDescCands candidates,
+            // partial rows as one-row RF tiles; one descriptor each
             const uint64_t u1 = stop - ubase;
             uint64_t u = n - ubase;
+            const uint64_t rmax = max((uint64_t)1, (uint64_t)kDescCands / R2);
             while (u < u1) {
+                if (emitted >= cap)
+                    return ubase + u;  // queue full: resume here in the next phase
                 const uint64_t d1 = (pop == OP_NONE) ? 0 : div_T(t, prsz, u);
                 const uint64_t rs = d1 * R2;
                 const uint32_t clo = (uint32_t)(u - rs);
                 if (clo != 0 || u1 - rs < R2) {
                     const uint32_t chi = (uint32_t)min((uint64_t)R2, u1 - rs);
-                    dispatch_rf<W, E>(p, st, pop, nt, xu, ubase, R2, off2, d1, 1, clo, chi, lane, ss.count);
+                    emit_tile<W, E>(p, od, 0, pop, nt, xu, ubase, R2, off2, d1, 1, clo, chi, lane, emitted);
                     u = rs + chi;
                 } else {
-                    const uint64_t nf = div_T(t, prsz, u1 - u);
-                    if (pop == OP_NONE || R2 >= kRFMin)
-                        dispatch_rf<W, E>(p, st, pop, nt, xu, ubase, R2, off2, d1, nf, 0, R2, lane, ss.count);
-                    else
-                        dispatch_cf<W, E>(p, st, pop, nt, xu, ubase, R2, off2, d1, nf, lane, ss.count);
+                    const uint64_t nf = min(div_T(t, prsz, u1 - u), rmax);
+                    emit_tile<W, E>(p, od, (pop == OP_NONE || R2 >= kRFMin) ? 0 : 1, pop, nt, xu, ubase, R2, off2, d1,
+                                    nf, 0, R2, lane, emitted);
                     u += nf * R2;
                 }
             }
@@ -1152,9 +1257,6 @@ __device__ __forceinline__ void flush_counts(const KParams &p, uint64_t my_count
     }
 }
 
-#ifndef SIMBA_UNIT_THREADS
-#define SIMBA_UNIT_THREADS 512
-#endif
 
 template <class W, int E>
 __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __grid_constant__ KParams p, const BlobInfo bi)
@@ -1181,39 +1283,107 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     uint64_t hint = p.nvirt / ((uint64_t)gridDim.x * (blockDim.x >> 5) * kGuide);
     if (hint < 1)
         hint = 1;
+    PlanShared *ps = plan_shared(p);
+    if (threadIdx.x == 0) {
+        ps->qn = 0;
+        ps->qnext = 0;
+        ps->active = 0;
+    }
+    __syncthreads();
+    // per-warp planning state, kept across phases
     Claim cl;
-    bool stop = false;
-    while (!stop && claim_run(p, t0, hint, cl)) {
-        for (uint64_t v = cl.v0; v < cl.v1 && !stop;) {
-            uint64_t c0, c1, vn;
-            run_piece(p, v, cl.v1, c0, c1, vn);
-            v = vn;
-            if (c0 >= c1)
-                continue;
-            if (early && c0 > read_best(p)) {
-                stop = true;
-                break;
-            }
-            od.reset();
-            uint64_t n = c0;
-            while (n < c1) {
-                SIMBA_CYC_BEGIN(co);
-                od.outer_at(n);
-                SIMBA_CYC_END(p, ST_CYC_OUTER, co);
-                const uint64_t pstop = min(od.pend, c1);
-                if (od.ovf_o) {
-                    ++ss.units;
-                    ++ss.rank_units;
-                    direct_range<W>(p, st, n, pstop, false, ss.count);
-                    n = pstop;
-                } else {
-                    n = run_pblock<W, E>(p, st, od, n, pstop, lane, ss);
+    bool have_claim = false, have_piece = false, done = false;
+    uint64_t v = 0, c0 = 0, c1 = 0, n = 0;
+    for (;;) {
+        // ---- plan: advance the odometer, queue up to kDescPerWarp tiles
+        int emitted = 0;
+        while (!done && emitted < kDescPerWarp) {
+            if (!have_piece) {
+                if (!have_claim || v >= cl.v1) {
+                    if (!claim_run(p, t0, hint, cl)) {
+                        done = true;
+                        break;
+                    }
+                    have_claim = true;
+                    v = cl.v0;
                 }
-                if (early && n < c1 && n > read_best(p))
-                    break;  // everything left in this piece ranks above a hit
+                uint64_t vn;
+                run_piece(p, v, cl.v1, c0, c1, vn);
+                v = vn;
+                if (c0 >= c1)
+                    continue;
+                if (early && c0 > read_best(p)) {
+                    done = true;  // claims ascend: everything left ranks above a hit
+                    break;
+                }
+                od.reset();
+                n = c0;
+                have_piece = true;
             }
-            vis += n - c0;
+            SIMBA_CYC_BEGIN(co);
+            od.outer_at(n);
+            SIMBA_CYC_END(p, ST_CYC_OUTER, co);
+            const uint64_t pstop = min(od.pend, c1);
+            if (od.ovf_o) {
+                ++ss.units;
+                ++ss.rank_units;
+                direct_range<W>(p, st, n, pstop, false, ss.count);
+                n = pstop;
+            } else {
+                n = plan_pblock<W, E>(p, st, od, n, pstop, lane, ss, emitted, kDescPerWarp);
+            }
+            if (n >= c1 || (early && n > read_best(p))) {  // piece finished (or the rest ranks above a hit)
+                vis += n - c0;
+                have_piece = false;
+            }
         }
+        if (lane == 0 && !done)
+            atomicAdd(&ps->active, 1u);
+        __syncthreads();
+        const unsigned int nq = ps->qn;
+        if (nq == 0 && ps->active == 0)
+            break;  // uniform: every warp is done and nothing is queued
+        // ---- sort the queue by tile variant (counting sort, warp 0)
+        if (threadIdx.x < 32) {
+            if (lane < kVariants)
+                ps->start[lane] = 0;
+            __syncwarp();
+            for (unsigned int i = lane; i < nq; i += 32)
+                atomicAdd(&ps->start[ps->var[i]], 1u);
+            __syncwarp();
+            if (lane == 0) {
+                unsigned int acc = 0;
+                for (int k = 0; k < kVariants; ++k) {
+                    const unsigned int c = ps->start[k];
+                    ps->start[k] = acc;
+                    acc += c;
+                }
+            }
+            __syncwarp();
+            for (unsigned int i = lane; i < nq; i += 32)
+                ps->order[atomicAdd(&ps->start[ps->var[i]], 1u)] = (uint16_t)i;
+        }
+        __syncthreads();
+        // ---- execute: all warps drain the queue variant by variant
+        const TileDesc<W, E> *q = desc_queue<W, E>(p);
+        for (;;) {
+            unsigned int idx = 0;
+            if (lane == 0)
+                idx = atomicAdd(&ps->qnext, 1u);
+            idx = __shfl_sync(FULL, idx, 0);
+            if (idx >= nq)
+                break;
+            exec_desc<W, E>(p, st, q + ps->order[idx], lane, ss.count);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ps->qn = 0;
+            ps->qnext = 0;
+            ps->active = 0;
+        }
+        if (lane == 0)
+            od.L->tac_gen = ~0u;  // the tiles reused the warp's block: refold next time
+        __syncthreads();
     }
     flush_counts(p, ss.count, vis, ss.units, ss.rank_units);
 }
@@ -1389,6 +1559,8 @@ struct simba_ctx {
     unsigned long long *h_ctr = nullptr;
     int32_t *d_tok = nullptr;
     unsigned long long *d_stats = nullptr;  // path statistics (SIMBA_STATS builds)
+    void *d_queue = nullptr;                // tile descriptors of the plan/execute phases
+    uint32_t qcap = 0, ps_off = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this context
 };
 
@@ -1560,6 +1732,9 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.units = c->d_ctr + 4;
     p.flags = reinterpret_cast<unsigned int *>(c->d_ctr + 6);
     p.stats = c->d_stats;
+    p.queue = c->d_queue;
+    p.qcap = c->qcap;
+    p.ps_off = c->ps_off;
     BlobInfo bi{c->d_blob, c->tbl_bytes, c->ex_bytes};
     const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(c->d_ctr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
@@ -1761,7 +1936,8 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         lv = (E == 1) ? sizeof(WarpLevels<uint64_t, 1>) : (E == 2) ? sizeof(WarpLevels<uint64_t, 2>)
                                                                  : sizeof(WarpLevels<uint64_t, 4>);
     const uint64_t ex_b = ((uint64_t)n * (k + 1) * c->wbytes + 15) & ~15ull;
-    const uint64_t other = sizeof(Tabs) + (ex_b <= 32 * 1024 ? ex_b : 0) + lv * (SIMBA_UNIT_THREADS / 32);
+    const uint64_t other =
+        sizeof(Tabs) + (ex_b <= 32 * 1024 ? ex_b : 0) + lv * (SIMBA_UNIT_THREADS / 32) + sizeof(PlanShared) + 16;
     const uint64_t tbl_cap = std::min<uint64_t>(160 * 1024, kSmemMax > other + 1024 ? kSmemMax - other - 1024 : 0);
     int R0 = o.r0;
     if (R0 == 0) {
@@ -1826,7 +2002,9 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     if (c->block_threads % 32 || c->block_threads < 32 || c->block_threads > SIMBA_UNIT_THREADS)
         return bail(fail(SIMBA_EINVAL, "block_threads must be a multiple of 32 in 32..%d", SIMBA_UNIT_THREADS));
     c->lvl_off = (uint32_t)(sizeof(Tabs) + c->tbl_bytes + (c->stage_examples ? c->ex_bytes : 0));
-    c->smem_unit = (int)(c->lvl_off + lv * (c->block_threads / 32));
+    c->ps_off = (uint32_t)((c->lvl_off + lv * (c->block_threads / 32) + 15) & ~(size_t)15);
+    c->smem_unit = (int)(c->ps_off + sizeof(PlanShared));
+    c->qcap = (uint32_t)(c->block_threads / 32 * kDescPerWarp);
     c->smem_direct = (int)(sizeof(Tabs) + (c->stage_examples ? c->ex_bytes : 0));
     // device state
     int ndev = 0;
@@ -1856,6 +2034,21 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         return cuda_bail(e, "cudaMalloc(counters)");
     if ((e = cudaMalloc(&c->d_tok, sizeof(int32_t) * MAXS)) != cudaSuccess)
         return cuda_bail(e, "cudaMalloc(tokens)");
+    {
+        size_t db = 0;
+        if (c->wbytes == 4)
+            db = (E == 1) ? sizeof(TileDesc<uint32_t, 1>) : (E == 2) ? sizeof(TileDesc<uint32_t, 2>)
+                                                                     : sizeof(TileDesc<uint32_t, 4>);
+        else
+            db = (E == 1) ? sizeof(TileDesc<uint64_t, 1>) : (E == 2) ? sizeof(TileDesc<uint64_t, 2>)
+                                                                     : sizeof(TileDesc<uint64_t, 4>);
+        int sms = 0;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess)
+            return cuda_bail(e, "cudaDeviceGetAttribute");
+        // one queue per resident CTA (at most two 256-thread CTAs per SM)
+        if ((e = cudaMalloc(&c->d_queue, db * c->qcap * (size_t)sms * 2)) != cudaSuccess)
+            return cuda_bail(e, "cudaMalloc(tile queue)");
+    }
     if ((e = cudaMalloc(&c->d_stats, sizeof(unsigned long long) * 2 * ST_N)) != cudaSuccess ||
         (e = cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 2 * ST_N, c->stream)) != cudaSuccess)
         return cuda_bail(e, "cudaMalloc(stats)");
@@ -1892,11 +2085,14 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     rc = (c->wbytes == 4) ? setup_kernels<uint32_t>(c) : setup_kernels<uint64_t>(c);
     if (rc)
         return bail(rc);
-    if (o.blocks_per_sm > 0) {
+    {
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-        c->grid_unit = std::min(c->grid_unit, sms * o.blocks_per_sm);
-        c->grid_direct = std::min(c->grid_direct, sms * o.blocks_per_sm);
+        if (o.blocks_per_sm > 0) {
+            c->grid_unit = std::min(c->grid_unit, sms * o.blocks_per_sm);
+            c->grid_direct = std::min(c->grid_direct, sms * o.blocks_per_sm);
+        }
+        c->grid_unit = std::min(c->grid_unit, sms * 2);  // the tile queue holds two CTAs per SM
     }
     *out = c;
     return SIMBA_OK;
@@ -1920,6 +2116,8 @@ void simba_ctx_destroy(simba_ctx *c)
         cudaFree(c->d_tok);
     if (c->d_stats)
         cudaFree(c->d_stats);
+    if (c->d_queue)
+        cudaFree(c->d_queue);
     if (c->h_ctr)
         cudaFreeHost(c->h_ctr);
     if (c->ev0)

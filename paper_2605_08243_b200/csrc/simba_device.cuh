@@ -89,6 +89,9 @@ struct KParams {
     unsigned long long *units;    // [0] units decoded, [1] units on the per-rank path
     unsigned int *flags;          // bit 0: stopped by the time budget
     unsigned long long *stats;    // [2*path] calls, [2*path+1] candidates (SIMBA_STATS builds)
+    void *queue;                  // tile descriptors, qcap per CTA (plan/execute phases)
+    uint32_t qcap;
+    uint32_t ps_off;              // shared-memory offset of the CTA's queue bookkeeping
 };
 
 // ---------------------------------------------------------------------------
@@ -491,6 +494,28 @@ struct TileArgs {
     int nres;
     bool fold;  // P folds too: one LOP3 per candidate
     Seg<W> res[MAXSO];
+};
+
+// Tile descriptor written by the planner (odometer) phase and consumed by the
+// execution phase of unit_kernel: everything a tile needs, so execution never
+// touches the odometer.  The per-example chains (E > 1) ride along for the
+// hit refinement.
+template <class W, int E>
+struct DescStash {
+    SegStash<W, E> s;
+};
+template <class W>
+struct DescStash<W, 1> {
+};
+
+template <class W, int E>
+struct __align__(16) TileDesc {
+    TileArgs<W> ta;        // folded outer test + residual chain (example 0)
+    Seg<W> sl[MAXSL];      // example 0's LEFT chain of the X unit
+    uint64_t ubase, row0, nrows, R1p;
+    uint32_t R2, off2, clo, chi, off1, offy;
+    int8_t pop, kind, nt, aff, x2d, pxop, sz1, szy;
+    DescStash<W, E> st;
 };
 
 template <class W, int E>
