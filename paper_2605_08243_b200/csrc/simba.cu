@@ -34,6 +34,26 @@
 #define SIMBA_UNIT_THREADS 512
 #endif
 
+// Debug builds (-DSIMBA_WATCHDOG): a warp still looping 3 s after the kernel
+// started reports where and traps, so a hang shows up as a located error.
+#ifdef SIMBA_WATCHDOG
+__device__ unsigned long long g_wd_t0;
+#define SIMBA_WD(tag, a, b)                                                                            \
+    do {                                                                                               \
+        unsigned long long now_;                                                                       \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                                       \
+        if (now_ - g_wd_t0 > 3000000000ull && g_wd_t0) {                                               \
+            printf("WD %s blk %d warp %d lane %d a=%llu b=%llu\n", tag, blockIdx.x, threadIdx.x >> 5,  \
+                   threadIdx.x & 31, (unsigned long long)(a), (unsigned long long)(b));                 \
+            __trap();                                                                                  \
+        }                                                                                              \
+    } while (0)
+#else
+#define SIMBA_WD(tag, a, b) \
+    do {                    \
+    } while (0)
+#endif
+
 using namespace simba;
 typedef unsigned __int128 u128;
 
@@ -350,6 +370,10 @@ struct SweepStats {
 // predicate (no candidate is skipped or grouped by value).
 
 constexpr uint32_t kRFMin = 128;  // RF tiles for rows of at least this many columns
+#ifndef SIMBA_CFSHORT
+#define SIMBA_CFSHORT 128
+#endif
+constexpr uint64_t kCFShort = SIMBA_CFSHORT;  // CF tiles with at most this many rows use 4 rows per lane
 
 template <class W>
 __device__ __forceinline__ bool is_low(W tm)
@@ -634,6 +658,78 @@ __device__ __forceinline__ uint32_t hitmask8(const W (&v)[8], W m, W c)
     return b;
 }
 
+// NJ-value variants for the CF tiles (NJ = 4 or 8 rows per lane)
+template <class W, int NJ>
+__device__ __forceinline__ bool hitNx4(const W (&v)[NJ], const W (&m)[4], const W (&c)[4])
+{
+    if constexpr (NJ == 8) {
+        return hit8x4<W>(v, m, c);
+    } else if constexpr (sizeof(W) == 4 && NJ == 4) {
+        uint32_t r;
+        asm("{\n\t.reg .pred p0, p1, p2, p3;\n\t.reg .b32 d;\n\t"
+            "lop3.b32 d, %1, %5, %9, 0x6a;\n\tsetp.ne.u32 p0, d, 0;\n\t"
+            "lop3.b32 d, %1, %6, %10, 0x6a;\n\tsetp.ne.u32 p1, d, 0;\n\t"
+            "lop3.b32 d, %1, %7, %11, 0x6a;\n\tsetp.ne.u32 p2, d, 0;\n\t"
+            "lop3.b32 d, %1, %8, %12, 0x6a;\n\tsetp.ne.u32 p3, d, 0;\n\t"
+            "lop3.and.b32 d|p0, %2, %5, %9, 0x6a, p0;\n\tlop3.and.b32 d|p1, %2, %6, %10, 0x6a, p1;\n\t"
+            "lop3.and.b32 d|p2, %2, %7, %11, 0x6a, p2;\n\tlop3.and.b32 d|p3, %2, %8, %12, 0x6a, p3;\n\t"
+            "lop3.and.b32 d|p0, %3, %5, %9, 0x6a, p0;\n\tlop3.and.b32 d|p1, %3, %6, %10, 0x6a, p1;\n\t"
+            "lop3.and.b32 d|p2, %3, %7, %11, 0x6a, p2;\n\tlop3.and.b32 d|p3, %3, %8, %12, 0x6a, p3;\n\t"
+            "lop3.and.b32 d|p0, %4, %5, %9, 0x6a, p0;\n\tlop3.and.b32 d|p1, %4, %6, %10, 0x6a, p1;\n\t"
+            "lop3.and.b32 d|p2, %4, %7, %11, 0x6a, p2;\n\tlop3.and.b32 d|p3, %4, %8, %12, 0x6a, p3;\n\t"
+            "and.pred p0, p0, p1;\n\tand.pred p2, p2, p3;\n\tand.pred p0, p0, p2;\n\t"
+            "selp.u32 %0, 0, 1, p0;\n\t}"
+            : "=r"(r)
+            : "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(m[0]), "r"(m[1]), "r"(m[2]), "r"(m[3]), "r"(c[0]),
+              "r"(c[1]), "r"(c[2]), "r"(c[3]));
+        return r != 0;
+    } else {
+        bool a = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+                a |= ((v[j] & m[k]) ^ c[k]) == 0;
+        return a;
+    }
+}
+
+template <class W, int NJ>
+__device__ __forceinline__ uint32_t hitmaskNx4(const W (&v)[NJ], const W (&m)[4], const W (&c)[4])
+{
+    uint32_t b = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            b |= (uint32_t)(((v[j] & m[k]) ^ c[k]) == 0) << (k * NJ + j);
+    return b;
+}
+
+template <class W, int NJ>
+__device__ __forceinline__ bool hitN(const W (&v)[NJ], W m, W c)
+{
+    if constexpr (NJ == 8) {
+        return hit8<W>(v, m, c);
+    } else {
+        bool a = false;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            a |= ((v[j] & m) ^ c) == 0;
+        return a;
+    }
+}
+
+template <class W, int NJ>
+__device__ __forceinline__ uint32_t hitmaskN(const W (&v)[NJ], W m, W c)
+{
+    uint32_t b = 0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+        b |= (uint32_t)(((v[j] & m) ^ c) == 0) << j;
+    return b;
+}
+
 // four consecutive (m, c) pairs from the tile buffer (16-byte aligned)
 template <class W>
 __device__ __forceinline__ void load4(const TPair<W> *pb, W (&m)[4], W (&c)[4])
@@ -777,6 +873,7 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
                     if (__any_sync(FULL, hit8(v, TM, TC))) {
                         uint32_t bits = hitmask8(v, TM, TC);
                         while (__any_sync(FULL, bits != 0)) {
+                            SIMBA_WD("rf1-slow", bits, c0);
                             const int b = bits ? __ffs(bits) - 1 : 0;
                             const uint32_t d2 = c0 + lane + 32 * b;
                             const bool h = bits != 0 && d2 < chi;
@@ -791,10 +888,52 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
     }
 }
 
+// One-row folded tile (partial rows at unit/claim boundaries, P = none):
+// columns [clo, chi) of row row0, 8 column values per lane, no padding rows.
+template <class W, int E>
+__device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int pop, XU xu, uint64_t ubase,
+                                       uint32_t R2, uint32_t off2, uint64_t row0, uint32_t clo, uint32_t chi,
+                                       int lane, uint64_t &my_count)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    WarpLevels<W, E> *L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
+    const SegStash<W, E> *sx = &L->stash;
+    const TileArgs<W> &ta = L->tac;
+    const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));
+    const W *g0 = reinterpret_cast<const W *>(p.gtbl);
+    W m = ta.tm, c = ta.tc;
+    if (pop != OP_NONE) {
+        Seg<W> slr[MAXSL];
+#pragma unroll
+        for (int i = 0; i < MAXSL; ++i)
+            slr[i] = L->sl0[i];
+        W xr[1];
+        rows_left<W, 1>(g0, xu, row0, 1, lane, slr, xr);
+        fold_p(pop, xr[0], true, ta.tm, ta.tc, m, c);
+    }
+    for (uint32_t c0 = clo; c0 < chi; c0 += 256) {
+        W s[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            s[j] = t0[off2 + c0 + lane + 32 * j];
+        if (__any_sync(FULL, hit8(s, m, c))) {
+            uint32_t bits = hitmask8(s, m, c);
+            while (__any_sync(FULL, bits != 0)) {
+                const int b = bits ? __ffs(bits) - 1 : 0;
+                const uint32_t d2 = c0 + lane + 32 * b;
+                const bool h = bits != 0 && d2 < chi;
+                bits &= bits - 1;
+                on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0, d2, my_count);
+            }
+        }
+    }
+    __syncwarp();
+}
+
 // CF tile: full rows [row0, row0 + nrows) x all R2 < TILE_BUF columns; lanes
 // hold 8 row values, columns are warp-uniform: per-column (m, c) (folded,
 // four columns per step) or per-column segments (GEN) in the buffer.
-template <class W, int E, int NT>
+template <class W, int E, int NT, int NJ>
 __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop, XU xu, uint64_t ubase,
                                      uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, int lane, uint64_t &my_count)
 {
@@ -841,19 +980,20 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop
         }
     }
     __syncwarp();
-    for (uint64_t rb = 0; rb < nrows; rb += 256) {
-        const uint32_t nb = (uint32_t)min((uint64_t)256, nrows - rb);
-        W x[8];
-        rows_left<W, 8>(g0, xu, row0 + rb, nb, lane, slr, x);  // rows past nb are masked at hit time
+    for (uint64_t rb = 0; rb < nrows; rb += 32 * NJ) {
+        const uint32_t nb = (uint32_t)min((uint64_t)(32 * NJ), nrows - rb);
+        W x[NJ];
+        rows_left<W, NJ>(g0, xu, row0 + rb, nb, lane, slr, x);  // rows past nb are masked at hit time
         if constexpr (NT == 0) {
             for (uint32_t cc = 0; cc < R4; cc += 4) {
                 W m[4], c[4];
                 load4(pb + cc, m, c);
-                if (__any_sync(FULL, hit8x4(x, m, c))) {
-                    uint32_t bits = hitmask8x4(x, m, c);
+                if (__any_sync(FULL, hitNx4<W, NJ>(x, m, c))) {
+                    uint32_t bits = hitmaskNx4<W, NJ>(x, m, c);
                     while (__any_sync(FULL, bits != 0)) {
+                        SIMBA_WD("cf-slow", bits, cc);
                         const int b = bits ? __ffs(bits) - 1 : 0;
-                        const uint32_t k = b >> 3, r = lane + 32 * (b & 7);
+                        const uint32_t k = b / NJ, r = lane + 32 * (b % NJ);
                         const bool h = bits != 0 && r < nb && cc + k < R2;
                         bits &= bits - 1;
                         on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc + k, my_count);
@@ -863,17 +1003,17 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop
         } else {
             for (uint32_t cc = 0; cc < R2; ++cc) {
                 const Seg<W> g = buf[cc];
-                W v[8];
+                W v[NJ];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < NJ; ++j) {
                     W u = seg_apply(g, x[j]);
 #pragma unroll
                     for (int i = 0; i < NT - 1; ++i)
                         u = seg_apply(res[i], u);
                     v[j] = u;
                 }
-                if (__any_sync(FULL, hit8(v, TM, TC))) {
-                    uint32_t bits = hitmask8(v, TM, TC);
+                if (__any_sync(FULL, hitN<W, NJ>(v, TM, TC))) {
+                    uint32_t bits = hitmaskN<W, NJ>(v, TM, TC);
                     while (__any_sync(FULL, bits != 0)) {
                         const int b = bits ? __ffs(bits) - 1 : 0;
                         const uint32_t r = lane + 32 * b;
@@ -903,7 +1043,9 @@ __device__ __forceinline__ void dispatch_rf(const KParams &p, const Staged &st, 
 {
     SIMBA_STAT(p, nrows == 1 ? ST_RF_ROW : nt == 0 ? ST_RF_FOLD : ST_RF_GEN, nrows * (chi - clo));
     SIMBA_CYC_BEGIN(ct);
-    if (nt == 0)
+    if (nt == 0 && nrows == 1)
+        tile_row1<W, E>(p, st, pop, xu, ubase, R2, off2, row0, clo, chi, lane, cnt);
+    else if (nt == 0)
         tile_rf<W, E, 0>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     else if (nt == 1)
         tile_rf<W, E, 1>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
@@ -923,16 +1065,25 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 {
     SIMBA_STAT(p, nt == 0 ? ST_CF_FOLD : ST_CF_GEN, nrows * R2);
     SIMBA_CYC_BEGIN(ct);
-    if (nt == 0)
-        tile_cf<W, E, 0>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
-    else if (nt == 1)
-        tile_cf<W, E, 1>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
-    else if (nt == 2)
-        tile_cf<W, E, 2>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
-    else if (nt == 3)
-        tile_cf<W, E, 3>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
-    else
-        tile_cf<W, E, 5>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+    if (nrows <= kCFShort) {  // 4 rows per lane: 128-row passes
+        if (nt == 0)
+            tile_cf<W, E, 0, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+        else if (nt == 1)
+            tile_cf<W, E, 1, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+        else if (nt == 2)
+            tile_cf<W, E, 2, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+        else
+            tile_cf<W, E, 5, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+    } else {
+        if (nt == 0)
+            tile_cf<W, E, 0, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+        else if (nt == 1)
+            tile_cf<W, E, 1, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+        else if (nt == 2)
+            tile_cf<W, E, 2, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+        else
+            tile_cf<W, E, 5, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+    }
     SIMBA_CYC_END(p, ST_CYC_TILE, ct);
 }
 
@@ -950,7 +1101,7 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 
 constexpr int kDescPerWarp = 24;
 constexpr uint64_t kDescCands = 1u << 16;  // candidates per descriptor (load balance)
-constexpr int kVariants = 8;
+constexpr int kVariants = 13;
 
 struct PlanShared {
     unsigned int qn, qnext, active;
@@ -971,9 +1122,12 @@ __device__ __forceinline__ TileDesc<W, E> *desc_queue(const KParams &p)
     return reinterpret_cast<TileDesc<W, E> *>(p.queue) + (size_t)blockIdx.x * p.qcap;
 }
 
-__device__ __forceinline__ int variant_of(int kind, int nt)
+__device__ __forceinline__ int variant_of(int kind, int nt, uint64_t nrows)
 {
-    return kind * 4 + (nt == 0 ? 0 : nt == 1 ? 1 : nt == 2 ? 2 : 3);
+    const int k = (nt == 0 ? 0 : nt == 1 ? 1 : nt == 2 ? 2 : 3);
+    if (kind == 0 && nt == 0 && nrows == 1)
+        return 12;  // tile_row1
+    return kind == 0 ? k : 4 + 2 * k + (nrows <= kCFShort ? 0 : 1);
 }
 
 template <class W, int E>
@@ -1010,7 +1164,7 @@ __device__ __forceinline__ void emit_tile(const KParams &p, const Odometer<W, E>
         d->pxop = (int8_t)xu.pxop;
         d->sz1 = (int8_t)xu.sz1;
         d->szy = (int8_t)xu.szy;
-        ps->var[slot] = (uint8_t)variant_of(kind, nt);
+        ps->var[slot] = (uint8_t)variant_of(kind, nt, nrows);
     }
     if constexpr (E > 1) {  // lane e holds example e's chains (hit refinement)
         if (lane < E) {
@@ -1083,7 +1237,10 @@ __device__ __forceinline__ uint64_t plan_pblock(const KParams &p, const Staged &
     const bool early = (p.mode == SIMBA_MODE_SEARCH);
     // tile description of this P block: folded outer test + residual chain,
     // cached per outer chain (sibling P blocks share it)
-    if (od.L->tac_gen != od.gen) {
+    unsigned int stale = 0;  // decided by lane 0: lane 0 rewrites tac_gen below
+    if (lane == 0)
+        stale = od.L->tac_gen != od.gen;
+    if (__shfl_sync(FULL, stale, 0)) {
         TileArgs<W> f;
         const W mask = (W)p.mask;
         f.nres = fold_outer(so, nso, (W)(y0 & mask), mask, f.tm, f.tc);
@@ -1284,6 +1441,10 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     if (hint < 1)
         hint = 1;
     PlanShared *ps = plan_shared(p);
+#ifdef SIMBA_WATCHDOG
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        g_wd_t0 = globaltimer_ns();
+#endif
     if (threadIdx.x == 0) {
         ps->qn = 0;
         ps->qnext = 0;
@@ -1296,8 +1457,10 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     uint64_t v = 0, c0 = 0, c1 = 0, n = 0;
     for (;;) {
         // ---- plan: advance the odometer, queue up to kDescPerWarp tiles
+        SIMBA_WD("phase", n, c1);
         int emitted = 0;
         while (!done && emitted < kDescPerWarp) {
+            SIMBA_WD("plan", n, emitted);
             if (!have_piece) {
                 if (!have_claim || v >= cl.v1) {
                     if (!claim_run(p, t0, hint, cl)) {
@@ -1373,6 +1536,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             idx = __shfl_sync(FULL, idx, 0);
             if (idx >= nq)
                 break;
+            SIMBA_WD("exec", idx, nq);
             exec_desc<W, E>(p, st, q + ps->order[idx], lane, ss.count);
         }
         __syncthreads();

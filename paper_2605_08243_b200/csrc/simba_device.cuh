@@ -618,6 +618,7 @@ struct Odometer {
         int sz = (no == 0) ? s : st.csz[no - 1];
         uint64_t rb = (no == 0) ? 0 : st.end[no - 1] - t->T[sz];
         uint64_t r = n - rb;
+        __syncwarp();  // every lane has read the stack before lane 0 pushes over it
         pop = OP_NONE;
         while (sz > R0) {
             const int op = find_slot(t, sz, r);
@@ -681,6 +682,7 @@ struct Odometer {
             int sz = (nx == 0) ? pj : st.csz[nx - 1];
             const uint64_t rb = (nx == 0) ? 0 : st.end[nx - 1] - t->T[sz];
             uint64_t r = q - rb;
+            __syncwarp();  // every lane has read the stack before lane 0 pushes over it
             x2d = false;
             while (sz > RG) {
                 const int op = find_slot(t, sz, r);
