@@ -23,3 +23,11 @@ def load_golden(name):
 @pytest.fixture(scope="session")
 def golden():
     return load_golden
+
+
+def pytest_collection_modifyitems(config, items):
+    """GPU tests get a per-test time limit (pytest-timeout, thread method) so a
+    device hang fails that test loudly instead of stalling the whole suite."""
+    for item in items:
+        if item.get_closest_marker("gpu") is not None and item.get_closest_marker("timeout") is None:
+            item.add_marker(pytest.mark.timeout(180, method="thread"))
