@@ -1099,13 +1099,21 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 // the odometer and the tiles (instruction-cache refills and register reloads
 // at every transition cost ~30% of the time).
 
-constexpr int kDescPerWarp = 24;
-constexpr uint64_t kDescCands = 1u << 16;  // candidates per descriptor (load balance)
+#ifndef SIMBA_DPW
+#define SIMBA_DPW 24
+#endif
+#ifndef SIMBA_DESC_LOG2
+#define SIMBA_DESC_LOG2 18
+#endif
+constexpr int kDescPerWarp = SIMBA_DPW;
+constexpr uint64_t kDescCands = 1ull << SIMBA_DESC_LOG2;  // candidates per descriptor (load balance)
 constexpr int kVariants = 13;
+constexpr int kSizeClasses = 4;  // per variant, largest descriptors first (shorter phase tails)
+constexpr int kBuckets = kVariants * kSizeClasses;
 
 struct PlanShared {
     unsigned int qn, qnext, active;
-    unsigned int start[kVariants];
+    unsigned int start[kBuckets];
     uint8_t var[SIMBA_UNIT_THREADS / 32 * kDescPerWarp];
     uint16_t order[SIMBA_UNIT_THREADS / 32 * kDescPerWarp];
 };
@@ -1164,7 +1172,9 @@ __device__ __forceinline__ void emit_tile(const KParams &p, const Odometer<W, E>
         d->pxop = (int8_t)xu.pxop;
         d->sz1 = (int8_t)xu.sz1;
         d->szy = (int8_t)xu.szy;
-        ps->var[slot] = (uint8_t)variant_of(kind, nt, nrows);
+        const uint64_t cands = nrows * (uint64_t)(chi - clo);
+        const int cls = cands >= (kDescCands >> 2) ? 0 : cands >= (kDescCands >> 5) ? 1 : cands >= 1024 ? 2 : 3;
+        ps->var[slot] = (uint8_t)(variant_of(kind, nt, nrows) * kSizeClasses + cls);
     }
     if constexpr (E > 1) {  // lane e holds example e's chains (hit refinement)
         if (lane < E) {
@@ -1508,15 +1518,15 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             break;  // uniform: every warp is done and nothing is queued
         // ---- sort the queue by tile variant (counting sort, warp 0)
         if (threadIdx.x < 32) {
-            if (lane < kVariants)
-                ps->start[lane] = 0;
+            for (int k = lane; k < kBuckets; k += 32)
+                ps->start[k] = 0;
             __syncwarp();
             for (unsigned int i = lane; i < nq; i += 32)
                 atomicAdd(&ps->start[ps->var[i]], 1u);
             __syncwarp();
             if (lane == 0) {
                 unsigned int acc = 0;
-                for (int k = 0; k < kVariants; ++k) {
+                for (int k = 0; k < kBuckets; ++k) {
                     const unsigned int c = ps->start[k];
                     ps->start[k] = acc;
                     acc += c;
