@@ -2110,18 +2110,37 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         lv = (E == 1) ? sizeof(WarpLevels<uint64_t, 1>) : (E == 2) ? sizeof(WarpLevels<uint64_t, 2>)
                                                                  : sizeof(WarpLevels<uint64_t, 4>);
     const uint64_t ex_b = ((uint64_t)n * (k + 1) * c->wbytes + 15) & ~15ull;
-    const uint64_t other =
-        sizeof(Tabs) + (ex_b <= 32 * 1024 ? ex_b : 0) + lv * (SIMBA_UNIT_THREADS / 32) + sizeof(PlanShared) + 16;
-    const uint64_t tbl_cap = std::min<uint64_t>(160 * 1024, kSmemMax > other + 1024 ? kSmemMax - other - 1024 : 0);
+    // shared-memory budget of the value table for a CTA of `warps` warps
+    auto table_cap = [&](int warps) -> uint64_t {
+        const uint64_t other =
+            sizeof(Tabs) + (ex_b <= 32 * 1024 ? ex_b : 0) + lv * (uint64_t)warps + sizeof(PlanShared) + 16;
+        return std::min<uint64_t>(160 * 1024, kSmemMax > other + 1024 ? kSmemMax - other - 1024 : 0);
+    };
+    auto largest_r0 = [&](uint64_t cap) {
+        int r0 = 1;
+        for (int r = 2; r <= max_size; ++r) {
+            if (t.T[r] > 65535 || (tbl_size(r) + kTblPad) * c->wbytes > cap)
+                break;
+            r0 = r;
+        }
+        return r0;
+    };
+    const int full_warps = SIMBA_UNIT_THREADS / 32;
+    const int req_warps = o.block_threads ? o.block_threads / 32 : 0;
+    int warps_hint = 0;  // 0: the default choice below
     int R0 = o.r0;
     if (R0 == 0) {
-        R0 = 1;
         // largest shared-memory table up to 160 KB: longer rows and fewer
-        // units beat a second CTA per SM (occupancy is register-bound anyway)
-        for (int r = 2; r <= max_size; ++r) {
-            if (t.T[r] > 65535 || (tbl_size(r) + kTblPad) * c->wbytes > tbl_cap)
-                break;
-            R0 = r;
+        // units beat a second CTA per SM (occupancy is register-bound anyway);
+        // when a 12-warp CTA admits a larger table than a 16-warp one
+        // (wide words, several table examples) it wins
+        R0 = largest_r0(table_cap(req_warps ? req_warps : full_warps));
+        if (!req_warps) {
+            const int r12 = largest_r0(table_cap(full_warps * 3 / 4));
+            if (r12 > R0) {
+                R0 = r12;
+                warps_hint = full_warps * 3 / 4;
+            }
         }
     } else {
         if (R0 < 1 || R0 > max_size)
@@ -2129,8 +2148,11 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         for (int r = 1; r <= R0; ++r)
             if (t.T[r] > 65535)
                 return bail(fail(SIMBA_EINVAL, "r0 %d: T[%d] exceeds 65535", R0, r));
-        if ((tbl_size(R0) + kTblPad) * c->wbytes > tbl_cap)
-            return bail(fail(SIMBA_EINVAL, "r0 %d: value table exceeds shared memory", R0));
+        if ((tbl_size(R0) + kTblPad) * c->wbytes > table_cap(req_warps ? req_warps : full_warps)) {
+            if (req_warps || (tbl_size(R0) + kTblPad) * c->wbytes > table_cap(full_warps * 3 / 4))
+                return bail(fail(SIMBA_EINVAL, "r0 %d: value table exceeds shared memory", R0));
+            warps_hint = full_warps * 3 / 4;
+        }
     }
     int RG = o.rg;
     if (RG == 0) {
@@ -2170,9 +2192,10 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     // 16 warps per SM either way (128 registers per thread): one 512-thread CTA
     // when the shared-memory tables do not leave room for two
     c->block_threads = o.block_threads ? o.block_threads
-                                       : ((sizeof(Tabs) + c->tbl_bytes + c->ex_bytes > 100 * 1024)
-                                              ? SIMBA_UNIT_THREADS
-                                              : (SIMBA_UNIT_THREADS > 256 ? SIMBA_UNIT_THREADS / 2 : 256));
+                       : warps_hint     ? warps_hint * 32
+                                        : ((sizeof(Tabs) + c->tbl_bytes + c->ex_bytes > 100 * 1024)
+                                               ? SIMBA_UNIT_THREADS
+                                               : (SIMBA_UNIT_THREADS > 256 ? SIMBA_UNIT_THREADS / 2 : 256));
     if (c->block_threads % 32 || c->block_threads < 32 || c->block_threads > SIMBA_UNIT_THREADS)
         return bail(fail(SIMBA_EINVAL, "block_threads must be a multiple of 32 in 32..%d", SIMBA_UNIT_THREADS));
     c->lvl_off = (uint32_t)(sizeof(Tabs) + c->tbl_bytes + (c->stage_examples ? c->ex_bytes : 0));
