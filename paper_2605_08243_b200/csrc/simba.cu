@@ -24,6 +24,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -1713,6 +1714,53 @@ int build_rows(int k, int max_size, std::vector<std::array<u128, 9>> &rows, int 
 
 }  // namespace
 
+namespace {
+
+// Process-wide pool of device arenas and pinned blocks, reused across
+// contexts (best fit, never shrunk): creating and destroying a context per
+// synthesize call must not pay cudaMalloc/cudaFree (which also synchronise).
+struct PoolBlock {
+    int device;
+    bool host;
+    size_t bytes;
+    void *ptr;
+};
+std::mutex g_pool_mu;
+std::vector<PoolBlock> g_pool;
+
+void *pool_get(int device, size_t bytes, bool host, size_t *got, cudaError_t *err)
+{
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        int best = -1;
+        for (int i = 0; i < (int)g_pool.size(); ++i) {
+            const PoolBlock &b = g_pool[i];
+            if (b.device == device && b.host == host && b.bytes >= bytes && (best < 0 || b.bytes < g_pool[best].bytes))
+                best = i;
+        }
+        if (best >= 0) {
+            void *p = g_pool[best].ptr;
+            *got = g_pool[best].bytes;
+            g_pool.erase(g_pool.begin() + best);
+            return p;
+        }
+    }
+    void *p = nullptr;
+    *err = host ? cudaMallocHost(&p, bytes) : cudaMalloc(&p, bytes);
+    if (*err != cudaSuccess)
+        return nullptr;
+    *got = bytes;
+    return p;
+}
+
+void pool_put(int device, void *p, size_t bytes, bool host)
+{
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back(PoolBlock{device, host, bytes, p});
+}
+
+}  // namespace
+
 struct simba_ctx {
     int device = 0, k = 0, w = 0, n = 0, max_size = 0;
     int wbytes = 4, R0 = 1, RG = 1, E = 1, kernel = 0;
@@ -1734,6 +1782,8 @@ struct simba_ctx {
     int32_t *d_tok = nullptr;
     unsigned long long *d_stats = nullptr;  // path statistics (SIMBA_STATS builds)
     void *d_queue = nullptr;                // tile descriptors of the plan/execute phases
+    void *arena = nullptr;                  // the pooled block all device buffers live in
+    size_t arena_bytes = 0;
     uint32_t qcap = 0, ps_off = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this context
 };
@@ -2221,17 +2271,10 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         return cuda_bail(e, "cudaStreamCreate");
     if ((e = cudaEventCreate(&c->ev0)) != cudaSuccess || (e = cudaEventCreate(&c->ev1)) != cudaSuccess)
         return cuda_bail(e, "cudaEventCreate");
-    if ((e = cudaMalloc(&c->d_tabs, sizeof(Tabs))) != cudaSuccess)
-        return cuda_bail(e, "cudaMalloc(tabs)");
-    if ((e = cudaMalloc(&c->d_blob, (size_t)c->tbl_bytes + c->ex_bytes)) != cudaSuccess)
-        return cuda_bail(e, "cudaMalloc(blob)");
-    if ((e = cudaMalloc(&c->d_gtbl, (size_t)c->E * c->gtbl_len * c->wbytes + 16)) != cudaSuccess)
-        return cuda_bail(e, "cudaMalloc(global value table)");
-    if ((e = cudaMalloc(&c->d_ctr, sizeof(unsigned long long) * kCtrWords)) != cudaSuccess)
-        return cuda_bail(e, "cudaMalloc(counters)");
-    if ((e = cudaMalloc(&c->d_tok, sizeof(int32_t) * MAXS)) != cudaSuccess)
-        return cuda_bail(e, "cudaMalloc(tokens)");
     {
+        // one device arena per context (tables, value tables, counters, tile
+        // queue) and one pinned counter block, both from a process-wide pool:
+        // cudaMalloc/cudaFree per synthesize call cost more than a small search
         size_t db = 0;
         if (c->wbytes == 4)
             db = (E == 1) ? sizeof(TileDesc<uint32_t, 1>) : (E == 2) ? sizeof(TileDesc<uint32_t, 2>)
@@ -2242,15 +2285,32 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         int sms = 0;
         if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess)
             return cuda_bail(e, "cudaDeviceGetAttribute");
-        // one queue per resident CTA (at most two 256-thread CTAs per SM)
-        if ((e = cudaMalloc(&c->d_queue, db * c->qcap * (size_t)sms * 2)) != cudaSuccess)
-            return cuda_bail(e, "cudaMalloc(tile queue)");
+        auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+        const size_t o_blob = up(sizeof(Tabs));
+        const size_t o_gtbl = up(o_blob + (size_t)c->tbl_bytes + c->ex_bytes);
+        const size_t o_ctr = up(o_gtbl + (size_t)c->E * c->gtbl_len * c->wbytes + 16);
+        const size_t o_tok = up(o_ctr + sizeof(unsigned long long) * kCtrWords);
+        const size_t o_stats = up(o_tok + sizeof(int32_t) * MAXS);
+        const size_t o_queue = up(o_stats + sizeof(unsigned long long) * 2 * ST_N);
+        const size_t total = up(o_queue + db * c->qcap * (size_t)sms * 2);  // two CTAs per SM at most
+        unsigned char *base = (unsigned char *)pool_get(c->device, total, false, &c->arena_bytes, &e);
+        if (!base)
+            return cuda_bail(e, "cudaMalloc(context arena)");
+        c->arena = base;
+        c->d_tabs = reinterpret_cast<Tabs *>(base);
+        c->d_blob = base + o_blob;
+        c->d_gtbl = base + o_gtbl;
+        c->d_ctr = reinterpret_cast<unsigned long long *>(base + o_ctr);
+        c->d_tok = reinterpret_cast<int32_t *>(base + o_tok);
+        c->d_stats = reinterpret_cast<unsigned long long *>(base + o_stats);
+        c->d_queue = base + o_queue;
+        if ((e = cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 2 * ST_N, c->stream)) != cudaSuccess)
+            return cuda_bail(e, "cudaMemsetAsync(stats)");
+        size_t hb = 0;
+        c->h_ctr = (unsigned long long *)pool_get(-1, sizeof(unsigned long long) * kCtrWords, true, &hb, &e);
+        if (!c->h_ctr)
+            return cuda_bail(e, "cudaMallocHost");
     }
-    if ((e = cudaMalloc(&c->d_stats, sizeof(unsigned long long) * 2 * ST_N)) != cudaSuccess ||
-        (e = cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 2 * ST_N, c->stream)) != cudaSuccess)
-        return cuda_bail(e, "cudaMalloc(stats)");
-    if ((e = cudaMallocHost(&c->h_ctr, sizeof(unsigned long long) * kCtrWords)) != cudaSuccess)
-        return cuda_bail(e, "cudaMallocHost");
     // examples as words W: inputs [n][k] then outputs [n]
     std::vector<unsigned char> ex(c->ex_bytes, 0);
     for (int i = 0; i < n * k; ++i) {
@@ -2299,24 +2359,14 @@ void simba_ctx_destroy(simba_ctx *c)
 {
     if (!c)
         return;
-    if (c->stream)
+    if (c->stream) {
         cudaSetDevice(c->device);
-    if (c->d_tabs)
-        cudaFree(c->d_tabs);
-    if (c->d_blob)
-        cudaFree(c->d_blob);
-    if (c->d_gtbl)
-        cudaFree(c->d_gtbl);
-    if (c->d_ctr)
-        cudaFree(c->d_ctr);
-    if (c->d_tok)
-        cudaFree(c->d_tok);
-    if (c->d_stats)
-        cudaFree(c->d_stats);
-    if (c->d_queue)
-        cudaFree(c->d_queue);
+        cudaStreamSynchronize(c->stream);  // nothing may still use the arena when it is reused
+    }
+    if (c->arena)
+        pool_put(c->device, c->arena, c->arena_bytes, false);
     if (c->h_ctr)
-        cudaFreeHost(c->h_ctr);
+        pool_put(-1, c->h_ctr, sizeof(unsigned long long) * kCtrWords, true);
     if (c->ev0)
         cudaEventDestroy(c->ev0);
     if (c->ev1)
