@@ -1214,6 +1214,9 @@ __device__ __noinline__ void exec_desc(const KParams &p, const Staged &st, const
         }
     }
     __syncwarp();
+#ifdef SIMBA_EMPTY_TILES
+    return;  // diagnostics: planning and queue traffic only
+#endif
     const XU xu{d->x2d, d->pxop, d->szy, d->sz1, d->offy, d->off1, d->R1p};
     if (d->kind == 0)
         dispatch_rf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, d->clo, d->chi,
