@@ -1104,7 +1104,7 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 #define SIMBA_DPW 24
 #endif
 #ifndef SIMBA_DESC_LOG2
-#define SIMBA_DESC_LOG2 18
+#define SIMBA_DESC_LOG2 17
 #endif
 constexpr int kDescPerWarp = SIMBA_DPW;
 constexpr uint64_t kDescCands = 1ull << SIMBA_DESC_LOG2;  // candidates per descriptor (load balance)
