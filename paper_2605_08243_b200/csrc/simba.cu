@@ -207,6 +207,24 @@ __device__ __noinline__ bool full_check(const KParams &p, const Staged &st, uint
     return true;
 }
 
+// Deferred verification (unit kernel): a candidate that survives the table
+// examples is queued for the reference-exact check, which all threads of the
+// CTA run together after the execution phase -- with dense hits a few tiles
+// would otherwise hold the whole CTA at the phase barrier.  Returns false when
+// the queue is full (the caller verifies inline) or in kernels without one.
+__device__ __forceinline__ bool defer_check(const KParams &p, uint64_t rank)
+{
+    if (!p.vq)
+        return false;
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned int *n = reinterpret_cast<unsigned int *>(smem + p.ps_off);  // PlanShared::vqn (first field)
+    const unsigned int slot = atomicAdd(n, 1u);
+    if (slot >= p.vqcap)
+        return false;
+    p.vq[(size_t)blockIdx.x * p.vqcap + slot] = rank;
+    return true;
+}
+
 // ===========================================================================
 // unit helpers
 // ===========================================================================
@@ -278,7 +296,7 @@ __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const S
     }
     if (hit) {
         const uint64_t rank = ubase + d1 * R2 + d2;
-        if (full_check<W>(p, st, rank))
+        if (!defer_check(p, rank) && full_check<W>(p, st, rank))
             record_hit(p, rank, my_count);
     }
 }
@@ -1107,12 +1125,14 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 #define SIMBA_DESC_LOG2 17
 #endif
 constexpr int kDescPerWarp = SIMBA_DPW;
+constexpr uint32_t kVerifyCap = 8192;  // deferred verifications per CTA and phase
 constexpr uint64_t kDescCands = 1ull << SIMBA_DESC_LOG2;  // candidates per descriptor (load balance)
 constexpr int kVariants = 13;
 constexpr int kSizeClasses = 4;  // per variant, largest descriptors first (shorter phase tails)
 constexpr int kBuckets = kVariants * kSizeClasses;
 
 struct PlanShared {
+    unsigned int vqn;  // deferred verifications queued this phase (must stay the first field)
     unsigned int qn, qnext, active;
     unsigned int start[kBuckets];
     uint8_t var[SIMBA_UNIT_THREADS / 32 * kDescPerWarp];
@@ -1460,6 +1480,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
         g_wd_t0 = globaltimer_ns();
 #endif
     if (threadIdx.x == 0) {
+        ps->vqn = 0;
         ps->qn = 0;
         ps->qnext = 0;
         ps->active = 0;
@@ -1554,6 +1575,17 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             exec_desc<W, E>(p, st, q + ps->order[idx], lane, ss.count);
         }
         __syncthreads();
+        // ---- verify the deferred candidates with every thread of the CTA
+        {
+            const unsigned int nv = min(ps->vqn, p.vqcap);
+            const unsigned long long *vq = p.vq + (size_t)blockIdx.x * p.vqcap;
+            for (unsigned int i = threadIdx.x; i < nv; i += blockDim.x)
+                if (full_check<W>(p, st, vq[i]))
+                    record_hit(p, vq[i], ss.count);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            ps->vqn = 0;
         if (threadIdx.x == 0) {
             ps->qn = 0;
             ps->qnext = 0;
@@ -1785,6 +1817,7 @@ struct simba_ctx {
     int32_t *d_tok = nullptr;
     unsigned long long *d_stats = nullptr;  // path statistics (SIMBA_STATS builds)
     void *d_queue = nullptr;                // tile descriptors of the plan/execute phases
+    unsigned long long *d_vq = nullptr;     // deferred verification queues
     void *arena = nullptr;                  // the pooled block all device buffers live in
     size_t arena_bytes = 0;
     uint32_t qcap = 0, ps_off = 0;
@@ -1962,6 +1995,8 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.queue = c->d_queue;
     p.qcap = c->qcap;
     p.ps_off = c->ps_off;
+    p.vq = direct ? nullptr : c->d_vq;  // the per-rank kernel verifies inline
+    p.vqcap = kVerifyCap;
     BlobInfo bi{c->d_blob, c->tbl_bytes, c->ex_bytes};
     const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(c->d_ctr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
@@ -2295,7 +2330,8 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         const size_t o_tok = up(o_ctr + sizeof(unsigned long long) * kCtrWords);
         const size_t o_stats = up(o_tok + sizeof(int32_t) * MAXS);
         const size_t o_queue = up(o_stats + sizeof(unsigned long long) * 2 * ST_N);
-        const size_t total = up(o_queue + db * c->qcap * (size_t)sms * 2);  // two CTAs per SM at most
+        const size_t o_vq = up(o_queue + db * c->qcap * (size_t)sms * 2);  // two CTAs per SM at most
+        const size_t total = up(o_vq + sizeof(unsigned long long) * kVerifyCap * (size_t)sms * 2);
         unsigned char *base = (unsigned char *)pool_get(c->device, total, false, &c->arena_bytes, &e);
         if (!base)
             return cuda_bail(e, "cudaMalloc(context arena)");
@@ -2307,6 +2343,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         c->d_tok = reinterpret_cast<int32_t *>(base + o_tok);
         c->d_stats = reinterpret_cast<unsigned long long *>(base + o_stats);
         c->d_queue = base + o_queue;
+        c->d_vq = reinterpret_cast<unsigned long long *>(base + o_vq);
         if ((e = cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 2 * ST_N, c->stream)) != cudaSuccess)
             return cuda_bail(e, "cudaMemsetAsync(stats)");
         size_t hb = 0;

@@ -92,6 +92,8 @@ struct KParams {
     void *queue;                  // tile descriptors, qcap per CTA (plan/execute phases)
     uint32_t qcap;
     uint32_t ps_off;              // shared-memory offset of the CTA's queue bookkeeping
+    unsigned long long *vq;       // deferred verification queue, vqcap ranks per CTA (null: verify inline)
+    uint32_t vqcap;
 };
 
 // ---------------------------------------------------------------------------
