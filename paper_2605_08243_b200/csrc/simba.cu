@@ -1126,6 +1126,10 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 #endif
 constexpr int kDescPerWarp = SIMBA_DPW;
 constexpr uint32_t kVerifyCap = 8192;  // deferred verifications per CTA and phase
+#ifndef SIMBA_SUPER_PER_SHARD
+#define SIMBA_SUPER_PER_SHARD 16
+#endif
+constexpr uint64_t kSuperPerShard = SIMBA_SUPER_PER_SHARD;  // round-robin super-chunks per shard
 constexpr uint64_t kDescCands = 1ull << SIMBA_DESC_LOG2;  // candidates per descriptor (load balance)
 constexpr int kVariants = 13;
 constexpr int kSizeClasses = 4;  // per variant, largest descriptors first (shorter phase tails)
@@ -1376,10 +1380,10 @@ struct Claim {
 };
 
 #ifndef SIMBA_GUIDE
-#define SIMBA_GUIDE 16
+#define SIMBA_GUIDE 8
 #endif
 #ifndef SIMBA_CHUNK_LOG2
-#define SIMBA_CHUNK_LOG2 20
+#define SIMBA_CHUNK_LOG2 16  // small last claims: short launch tails (multi-GPU shards)
 #endif
 constexpr uint64_t kGuide = SIMBA_GUIDE;  // claim ~ remaining / (warps * kGuide)
 
@@ -1945,7 +1949,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
             chunk <<= 1;
         spc = 1;
         if (rq.nshards > 1) {
-            const uint64_t per = range / (rq.nshards * 16) + 1;  // ~16 super-chunks per shard
+            const uint64_t per = range / (rq.nshards * kSuperPerShard) + 1;  // super-chunks per shard
             while (spc * chunk < per && spc < (1ull << 20))
                 spc <<= 1;
         } else {
