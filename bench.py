@@ -4,19 +4,20 @@
 Workload (BASELINE.json configs[4], "C5"): k=4 variables, w=32, n=10 examples,
 random outputs (unsatisfiable; the reference's full-sweep spec style,
 test_acceptance.py:278-289), exhaustive-count sweep of every size level 1..13
-(111,946,005,116 candidates per step).  One process per GPU (torchrun for
-N>1): each size level is sharded round-robin over the ranks and reduced with
-one all_reduce (SUM count, MIN first rank) per step -- the only exchange.
+(111,946,005,116 candidates per step) in ONE launch per step and rank: the
+levels' concatenated rank space (simba_run_levels) is sharded round-robin over
+the ranks (torchrun for N>1, one process per GPU) and reduced with one
+all_reduce per step -- the only exchange.
 
 value   device-timed whole-job candidates/s (CUDA events on the library
         stream, inputs resident, max over ranks)
 e2e     same metric through the public API with host buffers each step
         (context creation = H2D of spec + tables, per-spec value tables,
         scans, D2H of the results)
-roofline  INT32 issue roofline of the dominant launch (size 13): algorithmic
-        integer ops per launch (T[13] * 13 * e-bar) / its
-        CUDA-event duration, against the INT32 peak measured on this box by
-        simba_int32_peak (MEASURED_PEAKS.json has no integer figure)
+roofline  INT32 issue roofline of the step's launch: algorithmic integer ops
+        (sum_s T[s] * s * e-bar) / its CUDA-event duration,
+        against the INT32 peak measured on this box by simba_int32_peak
+        (MEASURED_PEAKS.json has no integer figure)
 cpu_baseline  the CPU oracle (oracle/simba_oracle.c, restatement of the
         reference path) on all host threads over a bounded size-13 sample
 
@@ -170,7 +171,7 @@ def run_reference(args):
 
 def config_dict(args):
     return {"workload": f"C5 exhaustive-count sweep, sizes 1..{args.size_bound}, k=4 w=32 n=10, "
-                        "random-output (unsat) spec; size levels sharded round-robin across ranks",
+                        "random-output (unsat) spec; all levels in one launch, sharded round-robin across ranks",
             "k": K, "w": W_BITS, "n_examples": N_PAIRS, "size_bound": args.size_bound,
             "parallelism": f"rank-space shards x{args.gpus}",
             "l2": "no flush needed: ~0 HBM bytes per candidate; value tables <= 80 MB built once per spec"}
@@ -238,28 +239,22 @@ def main():
 
     ctx = DeviceContext(spec, C, device=local)
     info = ctx.info()
-    scan = parallel.device_scan(ctx)
+    scan_levels = parallel.device_levels(ctx)
     stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
-    last_ms = {}
-    ex0 = {}
+    launch = {}
 
     def step():
-        levels = []
-        for s, t in enumerate(totals, start=1):
-            r = scan(s, 0, t, "count", rank, world, 0)
-            last_ms[s] = r.kernel_ms
-            ex0[s] = r.ex0_hits
-            levels.append((s, r))
-        if world > 1:  # exchange: SUM(count, visited), MIN(first) for all levels at once
-            cnt = torch.tensor([[r.count, r.visited] for _, r in levels], dtype=torch.int64, device=rdev)
-            fst = torch.tensor([r.best_rank if r.best_rank is not None else (1 << 63) - 1 for _, r in levels],
-                               dtype=torch.int64, device=rdev)
-            dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
-            dist.all_reduce(fst, op=dist.ReduceOp.MIN)
-            tot_visited = int(cnt[:, 1].sum().item())
-        else:
-            tot_visited = sum(r.visited for _, r in levels)
-        return tot_visited
+        # every size level 1..C in ONE launch per rank (this rank's round-robin
+        # shard of the levels' concatenated rank space), one reduction per step
+        r, levels = scan_levels(1, C, "count", rank, world)
+        launch["ms"] = r.kernel_ms
+        launch["ex0"] = r.ex0_hits
+        if world > 1:
+            tot = torch.tensor([sum(v for *_, v in levels), sum(c for _, c, _, _ in levels)], dtype=torch.int64,
+                               device=rdev)
+            dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+            return int(tot[0].item())
+        return sum(v for *_, v in levels)
 
     for _ in range(args.warmup):
         step()
@@ -272,11 +267,11 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    k13 = []
+    klaunch = []
     visited = 0
     for _ in range(args.steps):
         visited = step()
-        k13.append(last_ms[C])
+        klaunch.append(launch["ms"])
     torch.cuda.synchronize()
     e1.record(stream)
     torch.cuda.synchronize()
@@ -288,36 +283,37 @@ def main():
     assert visited == cands_per_step, (visited, cands_per_step)
     value = cands_per_step * args.steps / (dev_ms * 1e-3)
 
-    # dominant launch roofline: size C level (units kernel), INT32 issue peak
+    # roofline of the (only) launch of a step: all levels, INT32 issue peak
     peak_ops, peak_ms = C_double_pair(N, local)
-    ebar = 1.0 + ex0[C] / max(1, totals[C - 1] // world)
-    k_ms = statistics.mean(k13)
-    achieved = (totals[C - 1] / world) * C * ebar / (k_ms * 1e-3)
+    ebar = 1.0 + launch["ex0"] / max(1, cands_per_step // world)
+    k_ms = statistics.mean(klaunch)
+    algo_ops = sum(t * s for s, t in enumerate(totals, start=1)) / world * ebar  # sum over levels of T[s] * s
+    achieved = algo_ops / (k_ms * 1e-3)
     prof = profile_summary()
-    cand_s13 = (totals[C - 1] / world) / (k_ms * 1e-3)
+    cand_s = (cands_per_step / world) / (k_ms * 1e-3)
     roofline = {"bound": "int32", "achieved": achieved / 1e9, "peak": peak_ops / 1e9, "unit": "Gop/s",
                 "frac": achieved / peak_ops, "traffic": prof.get("dram_bytes_per_launch"),
-                "note": f"size-{C} unit_kernel launch: T[{C}]/N x {C} tokens x e-bar={ebar:.6f} integer ops "
-                        f"(SURVEY.md 8(d)) / {k_ms:.3f} ms (CUDA events); peak = simba_int32_peak LOP3+IMAD "
-                        "issue rate measured on this GPU (no integer figure in MEASURED_PEAKS.json). frac > 1 "
-                        "because shared subtrees are evaluated once per row/column, so the kernel spends "
-                        "~1 LOP3 per candidate instead of s*e-bar ops (DESIGN.md 2); see 'per_candidate' for "
-                        "the instruction-level view",
+                "note": f"the step's unit_kernel launch (levels 1..{C}): sum_s T[s]/N x s tokens x e-bar={ebar:.6f} "
+                        f"integer ops (SURVEY.md 8(d)) / {k_ms:.3f} ms (CUDA events); peak = simba_int32_peak "
+                        "LOP3+IMAD issue rate measured on this GPU (no integer figure in MEASURED_PEAKS.json). "
+                        "frac > 1 because shared subtrees are evaluated once per row/column, so the kernel spends "
+                        "~1 LOP3 per candidate instead of s*e-bar ops (DESIGN.md 2); see 'per_candidate' for the "
+                        "instruction-level view",
                 "per_candidate": {
-                    "test_ops_per_s": cand_s13 * ebar / 1e9,
-                    "frac_of_peak": cand_s13 * ebar / peak_ops,
+                    "test_ops_per_s": cand_s * ebar / 1e9,
+                    "frac_of_peak": cand_s * ebar / peak_ops,
                     "warp_inst_per_candidate": prof.get("warp_inst_per_candidate"),
                     "issue_active_pct": prof.get("issue_active_pct"),
                     "note": "one masked-compare (LOP3.PAND) test per candidate and example evaluated: "
                             "the floor of this algorithm; ncu fields from the committed profile "
-                            "(profiles/ncu_unit_kernel.json)"}}
+                            "(profiles/ncu_unit_kernel.json, the size-13 level launched alone)"}}
 
     # e2e through the public API: host spec -> context (H2D) -> scans -> D2H
     e2e = None
     if args.e2e_steps > 0:
         def e2e_step():
             c2 = DeviceContext(spec, C, device=local)
-            parallel.count_levels(parallel.device_scan(c2), totals, rank, world, device=rdev)
+            parallel.count_fused(parallel.device_levels(c2), C, rank, world, device=rdev)
             hb, db = c2.copied_bytes()
             c2.close()
             return hb, db
@@ -354,7 +350,7 @@ def main():
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
             "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
             "time_to_solve": tts,
-            "kernel": {"size13_launch_ms": k_ms, "e_bar": ebar, **info},
+            "kernel": {"launch_ms": k_ms, "launches_per_step": 1, "e_bar": ebar, **info},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

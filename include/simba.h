@@ -129,6 +129,25 @@ typedef struct {
 
 int simba_run(simba_ctx *ctx, const simba_range *req, simba_result *out);
 
+/* Several size levels in ONE launch (the loop of engine.py:222-262 fused on
+ * the device): levels size_lo..size_hi form one virtual rank space (level s
+ * follows level s-1), claimed in ascending order and sharded round-robin like
+ * simba_run.  SEARCH mode returns the minimum (size, rank) -- the smallest
+ * level with a hit, then its smallest rank, exactly the reference's order --
+ * and stops claiming above it; COUNT mode visits everything.  levels[i]
+ * (i = s - size_lo) receives the level's count, first satisfying rank and
+ * visited candidates (in SEARCH mode exact up to the found level); `out`
+ * carries the totals, the found (size, rank, tokens) and the launch time. */
+typedef struct {
+    int32_t size;
+    uint64_t count;
+    uint64_t first_rank;  /* SIMBA_NO_RANK if none */
+    uint64_t visited;
+} simba_level;
+
+int simba_run_levels(simba_ctx *ctx, int size_lo, int size_hi, int mode, uint64_t shard, uint64_t nshards,
+                     double time_budget_s, simba_level *levels, simba_result *out);
+
 /* engine.synthesize (engine.py:190-276), Algorithm 1 on the device: sizes
  * 1..size_bound ascending, each size level scanned in rank order (operator
  * blocks are contiguous rank ranges in slot order, engine.py:175-187) with

@@ -67,6 +67,15 @@ class Range(C.Structure):
     ]
 
 
+class Level(C.Structure):
+    _fields_ = [
+        ("size", C.c_int32),
+        ("count", C.c_uint64),
+        ("first_rank", C.c_uint64),
+        ("visited", C.c_uint64),
+    ]
+
+
 class Outcome(C.Structure):
     _fields_ = [
         ("status", C.c_int32),
@@ -92,6 +101,8 @@ SIGNATURES = {
     "simba_scan_range": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                    C.c_int, C.POINTER(Result)]),
     "simba_run": (C.c_int, [C.c_void_p, C.POINTER(Range), C.POINTER(Result)]),
+    "simba_run_levels": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_double,
+                                   C.POINTER(Level), C.POINTER(Result)]),
     "simba_synthesize": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_double, C.POINTER(Outcome)]),
     "simba_decode": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
     "simba_ctx_info": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int)] * 7),

@@ -83,6 +83,7 @@ int fail(int code, const char *fmt, ...)
 
 constexpr uint64_t kShuffleMult = 2246822507ULL;  // codec.py:29
 constexpr int kCtrWords = 8;  // ctr, best, count, visited, units[2], flags, spare
+constexpr int kLvlWords = 3 * (SIMBA_MAX_SIZE + 1);  // per-level count, visited, first rank
 constexpr uint64_t kSmemMax = 232448;  // opt-in dynamic shared memory per block (sm_100)
 constexpr uint64_t kTblPad = 256;      // words after the shared value table (8 x 32-lane reads)
 
@@ -148,10 +149,24 @@ __device__ __forceinline__ uint64_t shuffle_index(uint64_t i, uint64_t total)
     return (uint64_t)(((u128)i * kShuffleMult) % total);  // codec.py:232-236
 }
 
-__device__ __forceinline__ void record_hit(const KParams &p, uint64_t rank, uint64_t &my_count)
+// A verified hit at level s: the launch minimum is kept in virtual ranks
+// (lexicographic in (size, rank), the reference's order), per-level counts and
+// first ranks alongside.
+__device__ __forceinline__ void record_hit(const KParams &p, int s, uint64_t rank, uint64_t &my_count)
 {
     ++my_count;
-    atomicMin(p.best, (unsigned long long)rank);
+    atomicMin(p.best, (unsigned long long)(p.vbase[s] + rank));
+    atomicAdd(&p.lvl[s], 1ull);
+    atomicMin(&p.lvl[2 * (MAXS + 1) + s], (unsigned long long)rank);
+}
+
+// level of a virtual rank
+__device__ __forceinline__ int level_of(const KParams &p, uint64_t v)
+{
+    int s = p.s_lo;
+    while (s < p.s_hi && v >= p.vbase[s + 1])
+        ++s;
+    return s;
 }
 
 // One rank per lane over [n0, n1) (local indices when shuffled): reference
@@ -159,7 +174,7 @@ __device__ __forceinline__ void record_hit(const KParams &p, uint64_t rank, uint
 // lock-step with __any_sync early exit (expr.py:201-218 short-circuit).
 template <class W>
 __device__ __noinline__ void direct_range(const KParams &p, const Staged &st, uint64_t n0, uint64_t n1,
-                                          bool shuffled, uint64_t &my_count)
+                                          bool shuffled, uint64_t &my_count, int s)
 {
     const int lane = threadIdx.x & 31;
     const W *xs = reinterpret_cast<const W *>(st.xs);
@@ -173,8 +188,8 @@ __device__ __noinline__ void direct_range(const KParams &p, const Staged &st, ui
         uint64_t rank = 0;
         if (act) {
             rank = shuffled ? p.offset + shuffle_index(i, p.block_total) : i;
-            decode_tokens(st.t, rank, p.s, buf);
-            alive = (((eval_rpn<W, W>(buf, p.s, xs) ^ ys[0]) & mask) == 0);
+            decode_tokens(st.t, rank, s, buf);
+            alive = (((eval_rpn<W, W>(buf, s, xs) ^ ys[0]) & mask) == 0);
         }
         {
             const unsigned hits0 = __popc(__ballot_sync(FULL, alive));
@@ -185,24 +200,24 @@ __device__ __noinline__ void direct_range(const KParams &p, const Staged &st, ui
             if (!__any_sync(FULL, alive))
                 break;
             if (alive)
-                alive = (((eval_rpn<W, W>(buf, p.s, xs + (size_t)e * p.k) ^ ys[e]) & mask) == 0);
+                alive = (((eval_rpn<W, W>(buf, s, xs + (size_t)e * p.k) ^ ys[e]) & mask) == 0);
         }
         if (alive)
-            record_hit(p, rank, my_count);
+            record_hit(p, s, rank, my_count);
     }
 }
 
 // Reference-exact verification of one rank against every example.
 template <class W>
-__device__ __noinline__ bool full_check(const KParams &p, const Staged &st, uint64_t rank)
+__device__ __noinline__ bool full_check(const KParams &p, const Staged &st, uint64_t rank, int s)
 {
     const W *xs = reinterpret_cast<const W *>(st.xs);
     const W *ys = reinterpret_cast<const W *>(st.ys);
     const W mask = (W)p.mask;
     int8_t buf[MAXS];
-    decode_tokens(st.t, rank, p.s, buf);
+    decode_tokens(st.t, rank, s, buf);
     for (int e = 0; e < p.n; ++e)
-        if (((eval_rpn<W, W>(buf, p.s, xs + (size_t)e * p.k) ^ ys[e]) & mask) != 0)
+        if (((eval_rpn<W, W>(buf, s, xs + (size_t)e * p.k) ^ ys[e]) & mask) != 0)
             return false;
     return true;
 }
@@ -212,7 +227,7 @@ __device__ __noinline__ bool full_check(const KParams &p, const Staged &st, uint
 // CTA run together after the execution phase -- with dense hits a few tiles
 // would otherwise hold the whole CTA at the phase barrier.  Returns false when
 // the queue is full (the caller verifies inline) or in kernels without one.
-__device__ __forceinline__ bool defer_check(const KParams &p, uint64_t rank)
+__device__ __forceinline__ bool defer_check(const KParams &p, uint64_t vrank)
 {
     if (!p.vq)
         return false;
@@ -221,7 +236,7 @@ __device__ __forceinline__ bool defer_check(const KParams &p, uint64_t rank)
     const unsigned int slot = atomicAdd(n, 1u);
     if (slot >= p.vqcap)
         return false;
-    p.vq[(size_t)blockIdx.x * p.vqcap + slot] = rank;
+    p.vq[(size_t)blockIdx.x * p.vqcap + slot] = vrank;
     return true;
 }
 
@@ -265,7 +280,7 @@ __device__ __forceinline__ W left_input(const W *g, const XU &xu, uint64_t dy, u
 template <class W, int E>
 __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop, XU xu,
                                      uint64_t ubase, uint32_t R2, uint32_t off2, bool hit, uint64_t d1, uint32_t d2,
-                                     uint64_t &my_count)
+                                     uint64_t &my_count, int s)
 {
     const W *gtbl = reinterpret_cast<const W *>(p.gtbl);
     const W *ys = reinterpret_cast<const W *>(st.ys);
@@ -296,8 +311,8 @@ __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const S
     }
     if (hit) {
         const uint64_t rank = ubase + d1 * R2 + d2;
-        if (!defer_check(p, rank) && full_check<W>(p, st, rank))
-            record_hit(p, rank, my_count);
+        if (!defer_check(p, p.vbase[s] + rank) && full_check<W>(p, st, rank, s))
+            record_hit(p, s, rank, my_count);
     }
 }
 
@@ -800,7 +815,7 @@ __device__ __forceinline__ Seg<W> gen_seg(Seg<W> g, bool merge, const Seg<W> &r0
 template <class W, int E, int NT>
 __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop, XU xu, uint64_t ubase,
                                      uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, uint32_t clo,
-                                     uint32_t chi, int lane, uint64_t &my_count)
+                                     uint32_t chi, int lane, uint64_t &my_count, int lvl)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // this warp's shared block: folded outer chain, LEFT segments, tile buffer
@@ -873,7 +888,7 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
                             const uint32_t k = b >> 3, d2 = c0 + lane + 32 * (b & 7);
                             const bool h = bits != 0 && r + k < nr && d2 < chi;
                             bits &= bits - 1;
-                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r + k, d2, my_count);
+                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r + k, d2, my_count, lvl);
                         }
                     }
                 }
@@ -897,7 +912,7 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
                             const uint32_t d2 = c0 + lane + 32 * b;
                             const bool h = bits != 0 && d2 < chi;
                             bits &= bits - 1;
-                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, d2, my_count);
+                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, d2, my_count, lvl);
                         }
                     }
                 }
@@ -912,7 +927,7 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
 template <class W, int E>
 __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int pop, XU xu, uint64_t ubase,
                                        uint32_t R2, uint32_t off2, uint64_t row0, uint32_t clo, uint32_t chi,
-                                       int lane, uint64_t &my_count)
+                                       int lane, uint64_t &my_count, int lvl)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     WarpLevels<W, E> *L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
@@ -942,7 +957,7 @@ __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int p
                 const uint32_t d2 = c0 + lane + 32 * b;
                 const bool h = bits != 0 && d2 < chi;
                 bits &= bits - 1;
-                on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0, d2, my_count);
+                on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0, d2, my_count, lvl);
             }
         }
     }
@@ -954,7 +969,7 @@ __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int p
 // four columns per step) or per-column segments (GEN) in the buffer.
 template <class W, int E, int NT, int NJ>
 __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop, XU xu, uint64_t ubase,
-                                     uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, int lane, uint64_t &my_count)
+                                     uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, int lane, uint64_t &my_count, int lvl)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // this warp's shared block: folded outer chain, LEFT segments, tile buffer
@@ -1015,7 +1030,7 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop
                         const uint32_t k = b / NJ, r = lane + 32 * (b % NJ);
                         const bool h = bits != 0 && r < nb && cc + k < R2;
                         bits &= bits - 1;
-                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc + k, my_count);
+                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc + k, my_count, lvl);
                     }
                 }
             }
@@ -1038,7 +1053,7 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop
                         const uint32_t r = lane + 32 * b;
                         const bool h = bits != 0 && r < nb;
                         bits &= bits - 1;
-                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc, my_count);
+                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc, my_count, lvl);
                     }
                 }
             }
@@ -1058,50 +1073,51 @@ __device__ __forceinline__ int gen_nt(int pop, const TileArgs<W> &ta)
 template <class W, int E>
 __device__ __forceinline__ void dispatch_rf(const KParams &p, const Staged &st, int pop, int nt, const XU &xu,
                                             uint64_t ubase, uint32_t R2, uint32_t off2, uint64_t row0,
-                                            uint64_t nrows, uint32_t clo, uint32_t chi, int lane, uint64_t &cnt)
+                                            uint64_t nrows, uint32_t clo, uint32_t chi, int lane, uint64_t &cnt,
+                                            int lvl)
 {
     SIMBA_STAT(p, nrows == 1 ? ST_RF_ROW : nt == 0 ? ST_RF_FOLD : ST_RF_GEN, nrows * (chi - clo));
     SIMBA_CYC_BEGIN(ct);
     if (nt == 0 && nrows == 1)
-        tile_row1<W, E>(p, st, pop, xu, ubase, R2, off2, row0, clo, chi, lane, cnt);
+        tile_row1<W, E>(p, st, pop, xu, ubase, R2, off2, row0, clo, chi, lane, cnt, lvl);
     else if (nt == 0)
-        tile_rf<W, E, 0>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
+        tile_rf<W, E, 0>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt, lvl);
     else if (nt == 1)
-        tile_rf<W, E, 1>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
+        tile_rf<W, E, 1>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt, lvl);
     else if (nt == 2)
-        tile_rf<W, E, 2>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
+        tile_rf<W, E, 2>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt, lvl);
     else if (nt == 3)
-        tile_rf<W, E, 3>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
+        tile_rf<W, E, 3>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt, lvl);
     else
-        tile_rf<W, E, 5>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
+        tile_rf<W, E, 5>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt, lvl);
     SIMBA_CYC_END(p, ST_CYC_TILE, ct);
 }
 
 template <class W, int E>
 __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, int pop, int nt, const XU &xu,
                                             uint64_t ubase, uint32_t R2, uint32_t off2, uint64_t row0,
-                                            uint64_t nrows, int lane, uint64_t &cnt)
+                                            uint64_t nrows, int lane, uint64_t &cnt, int lvl)
 {
     SIMBA_STAT(p, nt == 0 ? ST_CF_FOLD : ST_CF_GEN, nrows * R2);
     SIMBA_CYC_BEGIN(ct);
     if (nrows <= kCFShort) {  // 4 rows per lane: 128-row passes
         if (nt == 0)
-            tile_cf<W, E, 0, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+            tile_cf<W, E, 0, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
         else if (nt == 1)
-            tile_cf<W, E, 1, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+            tile_cf<W, E, 1, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
         else if (nt == 2)
-            tile_cf<W, E, 2, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+            tile_cf<W, E, 2, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
         else
-            tile_cf<W, E, 5, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+            tile_cf<W, E, 5, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
     } else {
         if (nt == 0)
-            tile_cf<W, E, 0, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+            tile_cf<W, E, 0, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
         else if (nt == 1)
-            tile_cf<W, E, 1, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+            tile_cf<W, E, 1, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
         else if (nt == 2)
-            tile_cf<W, E, 2, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+            tile_cf<W, E, 2, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
         else
-            tile_cf<W, E, 5, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
+            tile_cf<W, E, 5, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
     }
     SIMBA_CYC_END(p, ST_CYC_TILE, ct);
 }
@@ -1197,6 +1213,7 @@ __device__ __forceinline__ void emit_tile(const KParams &p, const Odometer<W, E>
         d->pxop = (int8_t)xu.pxop;
         d->sz1 = (int8_t)xu.sz1;
         d->szy = (int8_t)xu.szy;
+        d->s = od.s;
         const uint64_t cands = nrows * (uint64_t)(chi - clo);
         const int cls = cands >= (kDescCands >> 2) ? 0 : cands >= (kDescCands >> 5) ? 1 : cands >= 1024 ? 2 : 3;
         ps->var[slot] = (uint8_t)(variant_of(kind, nt, nrows) * kSizeClasses + cls);
@@ -1244,9 +1261,9 @@ __device__ __noinline__ void exec_desc(const KParams &p, const Staged &st, const
     const XU xu{d->x2d, d->pxop, d->szy, d->sz1, d->offy, d->off1, d->R1p};
     if (d->kind == 0)
         dispatch_rf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, d->clo, d->chi,
-                          lane, cnt);
+                          lane, cnt, d->s);
     else
-        dispatch_cf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, lane, cnt);
+        dispatch_cf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, lane, cnt, d->s);
     __syncwarp();
 }
 
@@ -1330,7 +1347,7 @@ __device__ __forceinline__ uint64_t plan_pblock(const KParams &p, const Staged &
         if (od.ovf_l) {
             ++ss.rank_units;
             SIMBA_STAT(p, ST_DIRECT, stop - n);
-            direct_range<W>(p, st, n, stop, false, ss.count);
+            direct_range<W>(p, st, n, stop, false, ss.count, od.s);
         } else {
             // unit-local candidates u = d1 * R2 + d2 in [u0, u1): full rows in
             // RF (R2 >= kRFMin) or CF tiles of at most kDescCands candidates,
@@ -1357,7 +1374,7 @@ __device__ __forceinline__ uint64_t plan_pblock(const KParams &p, const Staged &
             }
         }
         n = stop;
-        if (early && n < n1 && n > read_best(p))
+        if (early && n < n1 && p.vbase[od.s] + n > read_best(p))
             break;  // everything left ranks above a hit
     }
     return n;
@@ -1466,9 +1483,9 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
         od.L->tac_gen = ~0u;
     __syncwarp();
     od.gt_e = reinterpret_cast<const W *>(p.gtbl) + (size_t)(lane & (E - 1)) * p.gtbl_len;
-    od.R0 = p.R0;
     od.RG = p.RG;
-    od.s = p.s;
+    od.s = p.s_lo;  // the level is (re)set per piece below
+    od.R0 = min(p.R0, od.s);
     od.lane = lane;
     od.ex = lane & (E - 1);
     const bool early = (p.mode == SIMBA_MODE_SEARCH);
@@ -1493,7 +1510,14 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     // per-warp planning state, kept across phases
     Claim cl;
     bool have_claim = false, have_piece = false, done = false;
-    uint64_t v = 0, c0 = 0, c1 = 0, n = 0;
+    uint64_t v = 0, c0 = 0, c1 = 0, n = 0;  // virtual ranks
+    int lvl_s = -1;        // level whose visited count is being accumulated
+    uint64_t lvl_vis = 0;
+    auto flush_level = [&]() {
+        if (lvl_s >= 0 && lvl_vis && lane == 0)
+            atomicAdd(&p.lvl[MAXS + 1 + lvl_s], (unsigned long long)lvl_vis);
+        lvl_vis = 0;
+    };
     for (;;) {
         // ---- plan: advance the odometer, queue up to kDescPerWarp tiles
         SIMBA_WD("phase", n, c1);
@@ -1522,18 +1546,35 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                 n = c0;
                 have_piece = true;
             }
+            // the level holding n: pieces may cross level boundaries
+            const int s = level_of(p, n);
+            if (s != od.s) {
+                od.s = s;
+                od.R0 = min(p.R0, s);
+                od.reset();
+            }
+            if (s != lvl_s) {
+                flush_level();
+                lvl_s = s;
+            }
+            const uint64_t vb = p.vbase[s];
+            const uint64_t rn = n - vb;  // in-size rank
+            const uint64_t rend = min(c1, p.vbase[s + 1]) - vb;
             SIMBA_CYC_BEGIN(co);
-            od.outer_at(n);
+            od.outer_at(rn);
             SIMBA_CYC_END(p, ST_CYC_OUTER, co);
-            const uint64_t pstop = min(od.pend, c1);
+            const uint64_t pstop = min(od.pend, rend);
+            uint64_t rn2;
             if (od.ovf_o) {
                 ++ss.units;
                 ++ss.rank_units;
-                direct_range<W>(p, st, n, pstop, false, ss.count);
-                n = pstop;
+                direct_range<W>(p, st, rn, pstop, false, ss.count, s);
+                rn2 = pstop;
             } else {
-                n = plan_pblock<W, E>(p, st, od, n, pstop, lane, ss, emitted, kDescPerWarp);
+                rn2 = plan_pblock<W, E>(p, st, od, rn, pstop, lane, ss, emitted, kDescPerWarp);
             }
+            lvl_vis += rn2 - rn;
+            n = vb + rn2;
             if (n >= c1 || (early && n > read_best(p))) {  // piece finished (or the rest ranks above a hit)
                 vis += n - c0;
                 have_piece = false;
@@ -1583,9 +1624,12 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
         {
             const unsigned int nv = min(ps->vqn, p.vqcap);
             const unsigned long long *vq = p.vq + (size_t)blockIdx.x * p.vqcap;
-            for (unsigned int i = threadIdx.x; i < nv; i += blockDim.x)
-                if (full_check<W>(p, st, vq[i]))
-                    record_hit(p, vq[i], ss.count);
+            for (unsigned int i = threadIdx.x; i < nv; i += blockDim.x) {
+                const int ls = level_of(p, vq[i]);
+                const uint64_t r = vq[i] - p.vbase[ls];
+                if (full_check<W>(p, st, r, ls))
+                    record_hit(p, ls, r, ss.count);
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0)
@@ -1599,6 +1643,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             od.L->tac_gen = ~0u;  // the tiles reused the warp's block: refold next time
         __syncthreads();
     }
+    flush_level();
     flush_counts(p, ss.count, vis, ss.units, ss.rank_units);
 }
 
@@ -1626,11 +1671,13 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS) direct_kernel(const __grid
                 stop = true;
                 break;
             }
-            direct_range<W>(p, st, c0, c1, p.shuffled != 0, my_count);
+            direct_range<W>(p, st, c0, c1, p.shuffled != 0, my_count, p.s);
             vis += c1 - c0;
         }
     }
     flush_counts(p, my_count, vis, 0, 0);
+    if ((threadIdx.x & 31) == 0 && vis)
+        atomicAdd(&p.lvl[MAXS + 1 + p.s], (unsigned long long)vis);
 }
 
 
@@ -1822,6 +1869,8 @@ struct simba_ctx {
     unsigned long long *d_stats = nullptr;  // path statistics (SIMBA_STATS builds)
     void *d_queue = nullptr;                // tile descriptors of the plan/execute phases
     unsigned long long *d_vq = nullptr;     // deferred verification queues
+    unsigned long long *d_lvl = nullptr;    // per-level count / visited / first rank of the last request
+    unsigned long long h_lvl[3 * (MAXS + 1)] = {};
     void *arena = nullptr;                  // the pooled block all device buffers live in
     size_t arena_bytes = 0;
     uint32_t qcap = 0, ps_off = 0;
@@ -1888,7 +1937,8 @@ void launch_scan(simba_ctx *c, const KParams &p, const BlobInfo &bi, bool direct
 uint64_t row_total(const simba_ctx *c, int s) { return (uint64_t)c->rows[s][8]; }
 
 struct Req {
-    int size;
+    int size;     // the (highest) level
+    int s_lo;     // fused request over levels [s_lo, size] (virtual ranks); 0: the single level `size`
     int mode;
     uint64_t lo, hi;  // local indices when shuffled, in-size ranks otherwise
     uint64_t chunk, shard, nshards, stop_above;
@@ -1917,7 +1967,24 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     out->completed = 1;
     if (rq.size < 1 || rq.size > c->max_size)
         return fail(SIMBA_ERANGE, "size %d outside 1..%d", rq.size, c->max_size);
-    const uint64_t tot = row_total(c, rq.size);
+    const int s_lo = rq.s_lo ? rq.s_lo : rq.size;
+    if (s_lo < 1 || s_lo > rq.size)
+        return fail(SIMBA_ERANGE, "levels %d..%d", s_lo, rq.size);
+    // virtual rank space of the levels [s_lo, size]
+    uint64_t vbase[MAXS + 2] = {};
+    {
+        unsigned __int128 acc = 0;
+        for (int z = s_lo; z <= rq.size; ++z) {
+            vbase[z] = (uint64_t)acc;
+            acc += row_total(c, z);
+        }
+        if (acc >> 64)
+            return fail(SIMBA_ERANGE, "levels %d..%d hold 2^64 ranks or more", s_lo, rq.size);
+        vbase[rq.size + 1] = (uint64_t)acc;
+    }
+    const uint64_t tot = vbase[rq.size + 1];
+    if (rq.s_lo && (rq.shuffled || rq.direct || c->kernel == 1))
+        return fail(SIMBA_EINVAL, "multi-level requests run on the unit kernel only");
     if (rq.shuffled) {
         if (rq.block_total == 0 || rq.offset > tot || rq.block_total > tot - rq.offset || rq.hi > rq.block_total)
             return fail(SIMBA_ERANGE, "block [%llu,+%llu) outside size %d", (unsigned long long)rq.offset,
@@ -1969,7 +2036,11 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.k = c->k;
     p.n = c->n;
     p.s = rq.size;
-    p.R0 = std::min(c->R0, rq.size);
+    p.R0 = c->R0;  // min(R0, s) per level in the kernel
+    p.s_lo = s_lo;
+    p.s_hi = rq.size;
+    memcpy(p.vbase, vbase, sizeof(vbase));
+    p.lvl = c->d_lvl;
     p.E = c->E;
     p.mode = rq.mode;
     p.shuffled = rq.shuffled ? 1 : 0;
@@ -2005,6 +2076,14 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(c->d_ctr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
     c->h2d_bytes += sizeof(init);
+    for (int z = 0; z <= MAXS; ++z) {  // per level: count, visited, first rank
+        c->h_lvl[z] = 0;
+        c->h_lvl[MAXS + 1 + z] = 0;
+        c->h_lvl[2 * (MAXS + 1) + z] = SIMBA_NO_RANK;
+    }
+    CK(cudaMemcpyAsync(c->d_lvl, c->h_lvl, sizeof(unsigned long long) * kLvlWords, cudaMemcpyHostToDevice,
+                       c->stream));
+    c->h2d_bytes += sizeof(unsigned long long) * kLvlWords;
     CK(cudaEventRecord(c->ev0, c->stream));
     if (c->wbytes == 4)
         launch_scan<uint32_t>(c, p, bi, direct);
@@ -2015,6 +2094,9 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(unsigned long long) * kCtrWords, cudaMemcpyDeviceToHost,
                        c->stream));
     c->d2h_bytes += sizeof(unsigned long long) * kCtrWords;
+    CK(cudaMemcpyAsync(c->h_lvl, c->d_lvl, sizeof(unsigned long long) * kLvlWords, cudaMemcpyDeviceToHost,
+                       c->stream));
+    c->d2h_bytes += sizeof(unsigned long long) * kLvlWords;
     CK(cudaStreamSynchronize(c->stream));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
@@ -2028,8 +2110,13 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     out->best_rank = c->h_ctr[1];
     out->completed = (c->h_ctr[6] & 1u) ? 0 : 1;
     out->found = out->best_rank != SIMBA_NO_RANK;
-    if (out->found) {
-        int rc = decode_rank(c, out->best_rank, rq.size, out->tokens);
+    if (out->found) {  // virtual -> (level, in-size rank)
+        int z = s_lo;
+        while (z < rq.size && out->best_rank >= vbase[z + 1])
+            ++z;
+        out->size = z;
+        out->best_rank -= vbase[z];
+        int rc = decode_rank(c, out->best_rank, z, out->tokens);
         if (rc)
             return rc;
         out->launches += 1;
@@ -2335,7 +2422,8 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         const size_t o_stats = up(o_tok + sizeof(int32_t) * MAXS);
         const size_t o_queue = up(o_stats + sizeof(unsigned long long) * 2 * ST_N);
         const size_t o_vq = up(o_queue + db * c->qcap * (size_t)sms * 2);  // two CTAs per SM at most
-        const size_t total = up(o_vq + sizeof(unsigned long long) * kVerifyCap * (size_t)sms * 2);
+        const size_t o_lvl = up(o_vq + sizeof(unsigned long long) * kVerifyCap * (size_t)sms * 2);
+        const size_t total = up(o_lvl + sizeof(unsigned long long) * kLvlWords);
         unsigned char *base = (unsigned char *)pool_get(c->device, total, false, &c->arena_bytes, &e);
         if (!base)
             return cuda_bail(e, "cudaMalloc(context arena)");
@@ -2348,6 +2436,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         c->d_stats = reinterpret_cast<unsigned long long *>(base + o_stats);
         c->d_queue = base + o_queue;
         c->d_vq = reinterpret_cast<unsigned long long *>(base + o_vq);
+        c->d_lvl = reinterpret_cast<unsigned long long *>(base + o_lvl);
         if ((e = cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 2 * ST_N, c->stream)) != cudaSuccess)
             return cuda_bail(e, "cudaMemsetAsync(stats)");
         size_t hb = 0;
@@ -2493,6 +2582,46 @@ int simba_run(simba_ctx *c, const simba_range *req, simba_result *out)
     return run_req(c, rq, out);
 }
 
+int simba_run_levels(simba_ctx *c, int size_lo, int size_hi, int mode, uint64_t shard, uint64_t nshards,
+                     double time_budget_s, simba_level *levels, simba_result *out)
+{
+    if (!c || !levels || !out)
+        return fail(SIMBA_EINVAL, "null argument");
+    if (mode != SIMBA_MODE_SEARCH && mode != SIMBA_MODE_COUNT)
+        return fail(SIMBA_EINVAL, "unknown mode %d", mode);
+    if (size_lo < 1 || size_hi < size_lo || size_hi > c->max_size)
+        return fail(SIMBA_ERANGE, "levels %d..%d outside 1..%d", size_lo, size_hi, c->max_size);
+    if (c->kernel == 1)
+        return fail(SIMBA_EINVAL, "multi-level requests run on the unit kernel only");
+    Req rq{};
+    rq.size = size_hi;
+    rq.s_lo = size_lo;
+    rq.mode = mode;
+    rq.lo = 0;
+    uint64_t tot = 0;
+    for (int z = size_lo; z <= size_hi; ++z) {
+        if (tot > UINT64_MAX - row_total(c, z))
+            return fail(SIMBA_ERANGE, "levels %d..%d hold 2^64 ranks or more", size_lo, size_hi);
+        tot += row_total(c, z);
+    }
+    rq.hi = tot;
+    rq.shard = shard;
+    rq.nshards = nshards ? nshards : 1;
+    rq.stop_above = SIMBA_NO_RANK;
+    rq.budget_s = time_budget_s;
+    const int rc = run_req(c, rq, out);
+    if (rc)
+        return rc;
+    for (int z = size_lo; z <= size_hi; ++z) {
+        simba_level &lv = levels[z - size_lo];
+        lv.size = z;
+        lv.count = c->h_lvl[z];
+        lv.visited = c->h_lvl[MAXS + 1 + z];
+        lv.first_rank = c->h_lvl[2 * (MAXS + 1) + z];
+    }
+    return SIMBA_OK;
+}
+
 int simba_synthesize(simba_ctx *c, int size_bound, int shuffled, double time_budget_s, simba_outcome *out)
 {
     if (!c)
@@ -2510,6 +2639,46 @@ int simba_synthesize(simba_ctx *c, int size_bound, int shuffled, double time_bud
     auto remaining = [&]() {
         return has_budget ? std::chrono::duration<double>(deadline - clk::now()).count() : -1.0;
     };
+    if (!shuffled && c->kernel != 1) {
+        // local order: all levels in one launch; the device returns the minimum
+        // (size, rank) and per-level visited counts (engine.py:222-262)
+        const auto t0 = clk::now();
+        std::vector<simba_level> lv(size_bound);
+        simba_result r{};
+        int rc = simba_run_levels(c, 1, size_bound, SIMBA_MODE_SEARCH, 0, 1, has_budget ? time_budget_s : -1.0,
+                                  lv.data(), &r);
+        if (rc)
+            return rc;
+        const double ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+        out->kernel_ms = r.kernel_ms;
+        out->launches = r.launches;
+        const int last = r.found ? r.size : size_bound;
+        uint64_t tot = 0;
+        for (int s = 1; s <= last; ++s)
+            tot += lv[s - 1].visited;
+        out->nsizes = last;
+        for (int s = 1; s <= last; ++s) {
+            out->visited[s - 1] = lv[s - 1].visited;
+            // one launch: its time apportioned to the levels by candidates
+            out->millis[s - 1] = tot ? ms * (double)lv[s - 1].visited / (double)tot : 0.0;
+        }
+        if (r.found) {
+            out->status = SIMBA_STATUS_FOUND;
+            out->size = r.size;
+            out->rank = r.best_rank;
+            memcpy(out->tokens, r.tokens, sizeof(out->tokens));
+        } else {
+            out->status = r.completed ? SIMBA_STATUS_NOT_FOUND : SIMBA_STATUS_TIMED_OUT;
+            if (!r.completed) {  // report the levels the budget reached
+                int reached = 0;
+                for (int s = 1; s <= size_bound; ++s)
+                    if (lv[s - 1].visited)
+                        reached = s;
+                out->nsizes = reached > 0 ? reached : 1;
+            }
+        }
+        return SIMBA_OK;
+    }
     for (int s = 1; s <= size_bound; ++s) {
         const auto t0 = clk::now();
         simba_result r{};

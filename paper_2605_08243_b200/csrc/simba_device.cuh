@@ -94,6 +94,11 @@ struct KParams {
     uint32_t ps_off;              // shared-memory offset of the CTA's queue bookkeeping
     unsigned long long *vq;       // deferred verification queue, vqcap ranks per CTA (null: verify inline)
     uint32_t vqcap;
+    // levels [s_lo, s_hi] of one launch in a virtual rank space: level s holds
+    // virtual ranks [vbase[s], vbase[s + 1]); lo/hi/best/stop_above are virtual
+    int s_lo, s_hi;
+    uint64_t vbase[MAXS + 2];
+    unsigned long long *lvl;      // per level: [s] count, [MAXS+1+s] visited, [2*(MAXS+1)+s] first rank
 };
 
 // ---------------------------------------------------------------------------
@@ -517,6 +522,7 @@ struct __align__(16) TileDesc {
     uint64_t ubase, row0, nrows, R1p;
     uint32_t R2, off2, clo, chi, off1, offy;
     int8_t pop, kind, nt, aff, x2d, pxop, sz1, szy;
+    int32_t s;             // expression size (level) of the tile
     DescStash<W, E> st;
 };
 

@@ -135,6 +135,7 @@ class RangeResult:
     units: int = 0
     rank_units: int = 0
     ex0_hits: int = 0
+    size: int = 0  # the level of best_rank (multi-level requests)
 
 
 @dataclass(frozen=True)
@@ -206,7 +207,7 @@ class DeviceContext:
             best_rank=r.best_rank if found else None,
             tokens=tuple(r.tokens[:size]) if found else None,
             completed=bool(r.completed), kernel_ms=r.kernel_ms, launches=r.launches,
-            units=r.units, rank_units=r.rank_units, ex0_hits=r.ex0_hits)
+            units=r.units, rank_units=r.rank_units, ex0_hits=r.ex0_hits, size=r.size)
 
     def scan_range(self, size, offset, block_total, start, stop, shuffled=False):
         """engine._scan_range (engine.py:128-156) -> (visited, best_rank, best_tokens)."""
@@ -225,6 +226,20 @@ class DeviceContext:
         r = N.Result()
         N.check_rc(N.lib.simba_run(self._ptr, C.byref(req), C.byref(r)))
         return self._result(r, size)
+
+    def run_levels(self, size_lo: int, size_hi: int, mode: str = "count", shard: int = 0, nshards: int = 1,
+                   time_budget: float | None = None):
+        """Levels size_lo..size_hi in one launch (simba_run_levels): returns
+        (RangeResult of the whole request -- its best_rank/tokens/size are the
+        minimum (size, rank) --, [(size, count, first_rank | None, visited)])."""
+        n = size_hi - size_lo + 1
+        lv = (N.Level * n)()
+        r = N.Result()
+        N.check_rc(N.lib.simba_run_levels(self._ptr, size_lo, size_hi,
+                                          N.MODE_SEARCH if mode == "search" else N.MODE_COUNT, shard, nshards,
+                                          -1.0 if time_budget is None else float(time_budget), lv, C.byref(r)))
+        levels = [(x.size, x.count, None if x.first_rank == N.NO_RANK else x.first_rank, x.visited) for x in lv]
+        return self._result(r, r.size), levels
 
     def count(self, size: int, lo: int = 0, hi: int | None = None, **kw) -> RangeResult:
         if hi is None:
@@ -303,10 +318,17 @@ def count_solutions(spec: Specification, table: CountTable, cfg: EngineConfig) -
     out = []
     with DeviceContext(spec, cfg.size_bound, device=cfg.device, r0=cfg.r0, rg=cfg.rg,
                        table_examples=cfg.table_examples, kernel=cfg.kernel) as ctx:
-        for s in range(1, cfg.size_bound + 1):
+        if cfg.kernel == "direct":  # the per-rank kernel runs one level per launch
+            for s in range(1, cfg.size_bound + 1):
+                t0 = time.perf_counter()
+                r = ctx.run(s, 0, table.total(s), mode="count")
+                out.append(SizeCount(s, r.count, r.best_rank, r.visited, (time.perf_counter() - t0) * 1e3))
+        else:  # every level in one launch; its time apportioned by candidates
             t0 = time.perf_counter()
-            r = ctx.run(s, 0, table.total(s), mode="count")
-            out.append(SizeCount(s, r.count, r.best_rank, r.visited, (time.perf_counter() - t0) * 1e3))
+            _, levels = ctx.run_levels(1, cfg.size_bound, mode="count")
+            ms = (time.perf_counter() - t0) * 1e3
+            tot = sum(v for *_, v in levels) or 1
+            out = [SizeCount(s, c, f, v, ms * v / tot) for s, c, f, v in levels]
     return tuple(out)
 
 

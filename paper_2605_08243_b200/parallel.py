@@ -77,6 +77,53 @@ def search(scan, totals, rank: int, world: int, chunk: int = 0, device=None, gro
     return None, None, levels
 
 
+def count_fused(scan_levels, size_bound: int, rank: int, world: int, device=None, group=None):
+    """Every level 1..size_bound in ONE device request per rank (simba_run_levels:
+    the levels' concatenated rank space sharded round-robin), then one SUM and
+    one MIN reduction for all levels together."""
+    _, levels = scan_levels(1, size_bound, "count", rank, world)
+    if world == 1:
+        return [LevelResult(s, c, f, v) for s, c, f, v in levels]
+    import torch
+    import torch.distributed as dist
+
+    sums = torch.tensor([[c, v] for _, c, _, v in levels], dtype=torch.int64, device=device)
+    mins = torch.tensor([_I64_MAX if f is None else f for _, _, f, _ in levels], dtype=torch.int64, device=device)
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(mins, op=dist.ReduceOp.MIN, group=group)
+    return [LevelResult(s, int(sums[i, 0].item()), None if int(mins[i].item()) == _I64_MAX else int(mins[i].item()),
+                        int(sums[i, 1].item())) for i, (s, *_) in enumerate(levels)]
+
+
+def search_fused(scan_levels, size_bound: int, rank: int, world: int, device=None, group=None):
+    """Algorithm 1 in one device request per rank: each shard returns its
+    minimum (size, rank); the job's answer is the lexicographic minimum over
+    shards (MIN of the size, then MIN of the rank among shards at that size)."""
+    r, levels = scan_levels(1, size_bound, "search", rank, world)
+    size = r.size if r.best_rank is not None else None
+    first = r.best_rank
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([_I64_MAX if size is None else size], dtype=torch.int64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        best_size = int(t.item())
+        t = torch.tensor([first if size is not None and size == best_size else _I64_MAX], dtype=torch.int64,
+                         device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        size = None if best_size == _I64_MAX else best_size
+        first = None if size is None else int(t.item())
+    return size, first, levels
+
+
+def device_levels(ctx):
+    """Adapter: DeviceContext.run_levels as a `scan_levels` callable."""
+    def scan_levels(size_lo, size_hi, mode, shard, nshards):
+        return ctx.run_levels(size_lo, size_hi, mode=mode, shard=shard, nshards=nshards)
+    return scan_levels
+
+
 def device_scan(ctx):
     """Adapter: DeviceContext.run as a `scan` callable."""
     def scan(size, lo, hi, mode, shard, nshards, chunk):

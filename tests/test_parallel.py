@@ -44,6 +44,24 @@ def oracle_scan(table, k, w, pairs):
     return scan
 
 
+def oracle_levels(table, k, w, pairs, chunk):
+    """Fused request emulated level by level with the same per-level shard
+    ownership (the reduction is what is under test)."""
+    scan = oracle_scan(table, k, w, pairs)
+
+    def scan_levels(size_lo, size_hi, mode, shard, nshards):
+        levels, found = [], None
+        for s in range(size_lo, size_hi + 1):
+            r = scan(s, 0, table.total(s), mode, shard, nshards, chunk)
+            levels.append((s, r.count, r.best_rank, r.visited))
+            if mode == "search" and r.best_rank is not None and found is None:
+                found = (s, r.best_rank)
+                break
+        res = SimpleNamespace(size=found[0] if found else size_hi, best_rank=found[1] if found else None)
+        return res, levels
+    return scan_levels
+
+
 def _worker(rank, world, port, cases, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -57,9 +75,14 @@ def _worker(rank, world, port, cases, out):
             if kind == "count":
                 lv = parallel.count_levels(scan, totals, rank, world, chunk=arg)
                 res.append([[x.size, x.count, x.first_rank, x.visited] for x in lv])
+                fused = parallel.count_fused(oracle_levels(table, spec["k"], spec["w"], pairs, arg), C, rank, world)
+                assert [[x.size, x.count, x.first_rank, x.visited] for x in fused] == res[-1]
             else:
                 size, first, lv = parallel.search(scan, totals, rank, world, chunk=arg)
                 res.append([size, first])
+                fs, ff, _ = parallel.search_fused(oracle_levels(table, spec["k"], spec["w"], pairs, arg), C, rank,
+                                                  world)
+                assert [fs, ff] == [size, first]
         out[rank] = res
     finally:
         dist.destroy_process_group()
