@@ -84,6 +84,7 @@ int fail(int code, const char *fmt, ...)
 constexpr uint64_t kShuffleMult = 2246822507ULL;  // codec.py:29
 constexpr int kCtrWords = 8;  // ctr, best, count, visited, units[2], flags, spare
 constexpr int kLvlWords = 3 * (SIMBA_MAX_SIZE + 1);  // per-level count, visited, first rank
+constexpr uint64_t kFuseCands = 1ull << 26;          // synthesize: levels fused per launch up to this many candidates
 constexpr uint64_t kSmemMax = 232448;  // opt-in dynamic shared memory per block (sm_100)
 constexpr uint64_t kTblPad = 256;      // words after the shared value table (8 x 32-lane reads)
 
@@ -2640,43 +2641,56 @@ int simba_synthesize(simba_ctx *c, int size_bound, int shuffled, double time_bud
         return has_budget ? std::chrono::duration<double>(deadline - clk::now()).count() : -1.0;
     };
     if (!shuffled && c->kernel != 1) {
-        // local order: all levels in one launch; the device returns the minimum
-        // (size, rank) and per-level visited counts (engine.py:222-262)
-        const auto t0 = clk::now();
-        std::vector<simba_level> lv(size_bound);
-        simba_result r{};
-        int rc = simba_run_levels(c, 1, size_bound, SIMBA_MODE_SEARCH, 0, 1, has_budget ? time_budget_s : -1.0,
-                                  lv.data(), &r);
-        if (rc)
-            return rc;
-        const double ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
-        out->kernel_ms = r.kernel_ms;
-        out->launches = r.launches;
-        const int last = r.found ? r.size : size_bound;
-        uint64_t tot = 0;
-        for (int s = 1; s <= last; ++s)
-            tot += lv[s - 1].visited;
-        out->nsizes = last;
-        for (int s = 1; s <= last; ++s) {
-            out->visited[s - 1] = lv[s - 1].visited;
-            // one launch: its time apportioned to the levels by candidates
-            out->millis[s - 1] = tot ? ms * (double)lv[s - 1].visited / (double)tot : 0.0;
-        }
-        if (r.found) {
-            out->status = SIMBA_STATUS_FOUND;
-            out->size = r.size;
-            out->rank = r.best_rank;
-            memcpy(out->tokens, r.tokens, sizeof(out->tokens));
-        } else {
-            out->status = r.completed ? SIMBA_STATUS_NOT_FOUND : SIMBA_STATUS_TIMED_OUT;
-            if (!r.completed) {  // report the levels the budget reached
-                int reached = 0;
-                for (int s = 1; s <= size_bound; ++s)
-                    if (lv[s - 1].visited)
-                        reached = s;
-                out->nsizes = reached > 0 ? reached : 1;
+        // local order: consecutive levels are fused into one launch while they
+        // hold at most kFuseCands candidates (small levels cost launch latency,
+        // not work); a large level runs alone so that an early hit is not
+        // followed by claims far above it.  Each launch returns the minimum
+        // (size, rank) of its levels and per-level visited counts.
+        int s_lo = 1;
+        while (s_lo <= size_bound) {
+            int s_hi = s_lo;
+            uint64_t acc = row_total(c, s_lo);
+            while (s_hi < size_bound && acc + row_total(c, s_hi + 1) <= kFuseCands)
+                acc += row_total(c, ++s_hi);
+            const auto t0 = clk::now();
+            std::vector<simba_level> lv(s_hi - s_lo + 1);
+            simba_result r{};
+            int rc = simba_run_levels(c, s_lo, s_hi, SIMBA_MODE_SEARCH, 0, 1,
+                                      has_budget ? std::max(0.0, remaining()) : -1.0, lv.data(), &r);
+            if (rc)
+                return rc;
+            const double ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+            out->kernel_ms += r.kernel_ms;
+            out->launches += r.launches;
+            const int last = r.found ? r.size : s_hi;
+            uint64_t tot = 0;
+            for (int z = s_lo; z <= last; ++z)
+                tot += lv[z - s_lo].visited;
+            int reached = s_lo;
+            for (int z = s_lo; z <= last; ++z) {
+                out->visited[z - 1] = lv[z - s_lo].visited;
+                // one launch: its time apportioned to its levels by candidates
+                out->millis[z - 1] = tot ? ms * (double)lv[z - s_lo].visited / (double)tot : 0.0;
+                if (lv[z - s_lo].visited)
+                    reached = z;
             }
+            if (r.found) {
+                out->nsizes = r.size;
+                out->status = SIMBA_STATUS_FOUND;
+                out->size = r.size;
+                out->rank = r.best_rank;
+                memcpy(out->tokens, r.tokens, sizeof(out->tokens));
+                return SIMBA_OK;
+            }
+            if (!r.completed || (has_budget && remaining() < 0)) {
+                out->nsizes = r.completed ? s_hi : reached;
+                out->status = SIMBA_STATUS_TIMED_OUT;
+                return SIMBA_OK;
+            }
+            out->nsizes = s_hi;
+            s_lo = s_hi + 1;
         }
+        out->status = SIMBA_STATUS_NOT_FOUND;
         return SIMBA_OK;
     }
     for (int s = 1; s <= size_bound; ++s) {
