@@ -16,4 +16,5 @@ with DeviceContext(spec, 13) as ctx:
         print(f"per-level launches {per:.2f} ms; fused {r.kernel_ms:.2f} ms visited ok {ok}", flush=True)
     for N in (2, 4, 8):
         ms = [ctx.run_levels(1, 13, "count", shard=i, nshards=N)[0].kernel_ms for i in range(N)]
-        print(f"fused N={N} shards max {max(ms):.2f} ms -> speedup {r.kernel_ms / max(ms):.2f}", flush=True)
+        print(f"fused N={N} shards {[round(m, 2) for m in ms]} max/mean {max(ms) * N / sum(ms):.3f} "
+              f"speedup {r.kernel_ms / max(ms):.2f}", flush=True)
