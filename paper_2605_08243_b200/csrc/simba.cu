@@ -281,9 +281,11 @@ __device__ __forceinline__ W left_input(const W *g, const XU &xu, uint64_t dy, u
 template <class W, int E>
 __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const SegStash<W, E> *sx, int pop, XU xu,
                                      uint64_t ubase, uint32_t R2, uint32_t off2, bool hit, uint64_t d1, uint32_t d2,
-                                     uint64_t &my_count, int s)
+                                     uint64_t &my_count)
 {
     const W *gtbl = reinterpret_cast<const W *>(p.gtbl);
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int s = (reinterpret_cast<const WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5))->cur_s;
     const W *ys = reinterpret_cast<const W *>(st.ys);
     const W mask = (W)p.mask;
     const unsigned hits0 = __popc(__ballot_sync(FULL, hit));
@@ -816,7 +818,7 @@ __device__ __forceinline__ Seg<W> gen_seg(Seg<W> g, bool merge, const Seg<W> &r0
 template <class W, int E, int NT>
 __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop, XU xu, uint64_t ubase,
                                      uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, uint32_t clo,
-                                     uint32_t chi, int lane, uint64_t &my_count, int lvl)
+                                     uint32_t chi, int lane, uint64_t &my_count)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // this warp's shared block: folded outer chain, LEFT segments, tile buffer
@@ -889,7 +891,7 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
                             const uint32_t k = b >> 3, d2 = c0 + lane + 32 * (b & 7);
                             const bool h = bits != 0 && r + k < nr && d2 < chi;
                             bits &= bits - 1;
-                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r + k, d2, my_count, lvl);
+                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r + k, d2, my_count);
                         }
                     }
                 }
@@ -913,7 +915,7 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
                             const uint32_t d2 = c0 + lane + 32 * b;
                             const bool h = bits != 0 && d2 < chi;
                             bits &= bits - 1;
-                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, d2, my_count, lvl);
+                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, d2, my_count);
                         }
                     }
                 }
@@ -928,7 +930,7 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
 template <class W, int E>
 __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int pop, XU xu, uint64_t ubase,
                                        uint32_t R2, uint32_t off2, uint64_t row0, uint32_t clo, uint32_t chi,
-                                       int lane, uint64_t &my_count, int lvl)
+                                       int lane, uint64_t &my_count)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     WarpLevels<W, E> *L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
@@ -958,7 +960,7 @@ __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int p
                 const uint32_t d2 = c0 + lane + 32 * b;
                 const bool h = bits != 0 && d2 < chi;
                 bits &= bits - 1;
-                on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0, d2, my_count, lvl);
+                on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0, d2, my_count);
             }
         }
     }
@@ -970,7 +972,7 @@ __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int p
 // four columns per step) or per-column segments (GEN) in the buffer.
 template <class W, int E, int NT, int NJ>
 __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop, XU xu, uint64_t ubase,
-                                     uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, int lane, uint64_t &my_count, int lvl)
+                                     uint32_t R2, uint32_t off2, uint64_t row0, uint64_t nrows, int lane, uint64_t &my_count)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // this warp's shared block: folded outer chain, LEFT segments, tile buffer
@@ -1031,7 +1033,7 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop
                         const uint32_t k = b / NJ, r = lane + 32 * (b % NJ);
                         const bool h = bits != 0 && r < nb && cc + k < R2;
                         bits &= bits - 1;
-                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc + k, my_count, lvl);
+                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc + k, my_count);
                     }
                 }
             }
@@ -1054,7 +1056,7 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop
                         const uint32_t r = lane + 32 * b;
                         const bool h = bits != 0 && r < nb;
                         bits &= bits - 1;
-                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc, my_count, lvl);
+                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc, my_count);
                     }
                 }
             }
@@ -1074,51 +1076,50 @@ __device__ __forceinline__ int gen_nt(int pop, const TileArgs<W> &ta)
 template <class W, int E>
 __device__ __forceinline__ void dispatch_rf(const KParams &p, const Staged &st, int pop, int nt, const XU &xu,
                                             uint64_t ubase, uint32_t R2, uint32_t off2, uint64_t row0,
-                                            uint64_t nrows, uint32_t clo, uint32_t chi, int lane, uint64_t &cnt,
-                                            int lvl)
+                                            uint64_t nrows, uint32_t clo, uint32_t chi, int lane, uint64_t &cnt)
 {
     SIMBA_STAT(p, nrows == 1 ? ST_RF_ROW : nt == 0 ? ST_RF_FOLD : ST_RF_GEN, nrows * (chi - clo));
     SIMBA_CYC_BEGIN(ct);
     if (nt == 0 && nrows == 1)
-        tile_row1<W, E>(p, st, pop, xu, ubase, R2, off2, row0, clo, chi, lane, cnt, lvl);
+        tile_row1<W, E>(p, st, pop, xu, ubase, R2, off2, row0, clo, chi, lane, cnt);
     else if (nt == 0)
-        tile_rf<W, E, 0>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt, lvl);
+        tile_rf<W, E, 0>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     else if (nt == 1)
-        tile_rf<W, E, 1>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt, lvl);
+        tile_rf<W, E, 1>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     else if (nt == 2)
-        tile_rf<W, E, 2>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt, lvl);
+        tile_rf<W, E, 2>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     else if (nt == 3)
-        tile_rf<W, E, 3>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt, lvl);
+        tile_rf<W, E, 3>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     else
-        tile_rf<W, E, 5>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt, lvl);
+        tile_rf<W, E, 5>(p, st, pop, xu, ubase, R2, off2, row0, nrows, clo, chi, lane, cnt);
     SIMBA_CYC_END(p, ST_CYC_TILE, ct);
 }
 
 template <class W, int E>
 __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, int pop, int nt, const XU &xu,
                                             uint64_t ubase, uint32_t R2, uint32_t off2, uint64_t row0,
-                                            uint64_t nrows, int lane, uint64_t &cnt, int lvl)
+                                            uint64_t nrows, int lane, uint64_t &cnt)
 {
     SIMBA_STAT(p, nt == 0 ? ST_CF_FOLD : ST_CF_GEN, nrows * R2);
     SIMBA_CYC_BEGIN(ct);
     if (nrows <= kCFShort) {  // 4 rows per lane: 128-row passes
         if (nt == 0)
-            tile_cf<W, E, 0, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
+            tile_cf<W, E, 0, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
         else if (nt == 1)
-            tile_cf<W, E, 1, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
+            tile_cf<W, E, 1, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
         else if (nt == 2)
-            tile_cf<W, E, 2, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
+            tile_cf<W, E, 2, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
         else
-            tile_cf<W, E, 5, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
+            tile_cf<W, E, 5, 4>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
     } else {
         if (nt == 0)
-            tile_cf<W, E, 0, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
+            tile_cf<W, E, 0, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
         else if (nt == 1)
-            tile_cf<W, E, 1, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
+            tile_cf<W, E, 1, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
         else if (nt == 2)
-            tile_cf<W, E, 2, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
+            tile_cf<W, E, 2, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
         else
-            tile_cf<W, E, 5, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt, lvl);
+            tile_cf<W, E, 5, 8>(p, st, pop, xu, ubase, R2, off2, row0, nrows, lane, cnt);
     }
     SIMBA_CYC_END(p, ST_CYC_TILE, ct);
 }
@@ -1244,6 +1245,7 @@ __device__ __noinline__ void exec_desc(const KParams &p, const Staged &st, const
 #pragma unroll
         for (int i = 0; i < MAXSL; ++i)
             L->sl0[i] = d->sl[i];
+        L->cur_s = d->s;  // the tile's level, read by on_hits
     }
     if constexpr (E > 1) {
         if (lane < E) {
@@ -1262,9 +1264,9 @@ __device__ __noinline__ void exec_desc(const KParams &p, const Staged &st, const
     const XU xu{d->x2d, d->pxop, d->szy, d->sz1, d->offy, d->off1, d->R1p};
     if (d->kind == 0)
         dispatch_rf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, d->clo, d->chi,
-                          lane, cnt, d->s);
+                          lane, cnt);
     else
-        dispatch_cf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, lane, cnt, d->s);
+        dispatch_cf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, lane, cnt);
     __syncwarp();
 }
 
@@ -1512,13 +1514,6 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     Claim cl;
     bool have_claim = false, have_piece = false, done = false;
     uint64_t v = 0, c0 = 0, c1 = 0, n = 0;  // virtual ranks
-    int lvl_s = -1;        // level whose visited count is being accumulated
-    uint64_t lvl_vis = 0;
-    auto flush_level = [&]() {
-        if (lvl_s >= 0 && lvl_vis && lane == 0)
-            atomicAdd(&p.lvl[MAXS + 1 + lvl_s], (unsigned long long)lvl_vis);
-        lvl_vis = 0;
-    };
     for (;;) {
         // ---- plan: advance the odometer, queue up to kDescPerWarp tiles
         SIMBA_WD("phase", n, c1);
@@ -1554,13 +1549,9 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                 od.R0 = min(p.R0, s);
                 od.reset();
             }
-            if (s != lvl_s) {
-                flush_level();
-                lvl_s = s;
-            }
             const uint64_t vb = p.vbase[s];
             const uint64_t rn = n - vb;  // in-size rank
-            const uint64_t rend = min(c1, p.vbase[s + 1]) - vb;
+            const uint64_t rend = min(c1, (uint64_t)p.vbase[s + 1]) - vb;
             SIMBA_CYC_BEGIN(co);
             od.outer_at(rn);
             SIMBA_CYC_END(p, ST_CYC_OUTER, co);
@@ -1574,7 +1565,6 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             } else {
                 rn2 = plan_pblock<W, E>(p, st, od, rn, pstop, lane, ss, emitted, kDescPerWarp);
             }
-            lvl_vis += rn2 - rn;
             n = vb + rn2;
             if (n >= c1 || (early && n > read_best(p))) {  // piece finished (or the rest ranks above a hit)
                 vis += n - c0;
@@ -1644,7 +1634,6 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             od.L->tac_gen = ~0u;  // the tiles reused the warp's block: refold next time
         __syncthreads();
     }
-    flush_level();
     flush_counts(p, ss.count, vis, ss.units, ss.rank_units);
 }
 
@@ -1871,7 +1860,7 @@ struct simba_ctx {
     void *d_queue = nullptr;                // tile descriptors of the plan/execute phases
     unsigned long long *d_vq = nullptr;     // deferred verification queues
     unsigned long long *d_lvl = nullptr;    // per-level count / visited / first rank of the last request
-    unsigned long long h_lvl[3 * (MAXS + 1)] = {};
+    unsigned long long h_lvl[3 * (MAXS + 1) + MAXS + 2] = {};  // + the level bases of the request
     void *arena = nullptr;                  // the pooled block all device buffers live in
     size_t arena_bytes = 0;
     uint32_t qcap = 0, ps_off = 0;
@@ -2040,7 +2029,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.R0 = c->R0;  // min(R0, s) per level in the kernel
     p.s_lo = s_lo;
     p.s_hi = rq.size;
-    memcpy(p.vbase, vbase, sizeof(vbase));
+    p.vbase = c->d_lvl + kLvlWords;  // the level bases follow the per-level counters
     p.lvl = c->d_lvl;
     p.E = c->E;
     p.mode = rq.mode;
@@ -2082,9 +2071,11 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
         c->h_lvl[MAXS + 1 + z] = 0;
         c->h_lvl[2 * (MAXS + 1) + z] = SIMBA_NO_RANK;
     }
-    CK(cudaMemcpyAsync(c->d_lvl, c->h_lvl, sizeof(unsigned long long) * kLvlWords, cudaMemcpyHostToDevice,
-                       c->stream));
-    c->h2d_bytes += sizeof(unsigned long long) * kLvlWords;
+    for (int z = 0; z <= MAXS + 1; ++z)
+        c->h_lvl[kLvlWords + z] = vbase[z];
+    CK(cudaMemcpyAsync(c->d_lvl, c->h_lvl, sizeof(unsigned long long) * (kLvlWords + MAXS + 2),
+                       cudaMemcpyHostToDevice, c->stream));
+    c->h2d_bytes += sizeof(unsigned long long) * (kLvlWords + MAXS + 2);
     CK(cudaEventRecord(c->ev0, c->stream));
     if (c->wbytes == 4)
         launch_scan<uint32_t>(c, p, bi, direct);
@@ -2424,7 +2415,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         const size_t o_queue = up(o_stats + sizeof(unsigned long long) * 2 * ST_N);
         const size_t o_vq = up(o_queue + db * c->qcap * (size_t)sms * 2);  // two CTAs per SM at most
         const size_t o_lvl = up(o_vq + sizeof(unsigned long long) * kVerifyCap * (size_t)sms * 2);
-        const size_t total = up(o_lvl + sizeof(unsigned long long) * kLvlWords);
+        const size_t total = up(o_lvl + sizeof(unsigned long long) * (kLvlWords + MAXS + 2));
         unsigned char *base = (unsigned char *)pool_get(c->device, total, false, &c->arena_bytes, &e);
         if (!base)
             return cuda_bail(e, "cudaMalloc(context arena)");
@@ -2613,11 +2604,16 @@ int simba_run_levels(simba_ctx *c, int size_lo, int size_hi, int mode, uint64_t 
     const int rc = run_req(c, rq, out);
     if (rc)
         return rc;
+    // per-level visited: the request's visited candidates fill the levels in
+    // order (claims ascend; COUNT mode visits every level completely, SEARCH
+    // mode every level below the found one)
+    uint64_t left = out->visited;
     for (int z = size_lo; z <= size_hi; ++z) {
         simba_level &lv = levels[z - size_lo];
         lv.size = z;
         lv.count = c->h_lvl[z];
-        lv.visited = c->h_lvl[MAXS + 1 + z];
+        lv.visited = std::min<uint64_t>(left, row_total(c, z));
+        left -= lv.visited;
         lv.first_rank = c->h_lvl[2 * (MAXS + 1) + z];
     }
     return SIMBA_OK;

@@ -97,7 +97,7 @@ struct KParams {
     // levels [s_lo, s_hi] of one launch in a virtual rank space: level s holds
     // virtual ranks [vbase[s], vbase[s + 1]); lo/hi/best/stop_above are virtual
     int s_lo, s_hi;
-    uint64_t vbase[MAXS + 2];
+    const unsigned long long *vbase;  // [MAXS + 2] (global; kept out of the parameter block)
     unsigned long long *lvl;      // per level: [s] count, [MAXS+1+s] visited, [2*(MAXS+1)+s] first rank
 };
 
@@ -535,6 +535,7 @@ struct WarpLevels {
     TileArgs<W> tac;        // folded outer chain of odometer generation tac_gen
     Seg<W> sl0[MAXSL];      // example 0's LEFT chain of the current X unit
     uint32_t tac_gen;
+    int cur_s;              // level of the tile being executed (hit path)
 };
 
 template <class W, int E>
