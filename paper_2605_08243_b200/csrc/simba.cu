@@ -1517,6 +1517,8 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     for (;;) {
         // ---- plan: advance the odometer, queue up to kDescPerWarp tiles
         SIMBA_WD("phase", n, c1);
+        SIMBA_CYC_BEGIN(cph);
+        SIMBA_CYC_BEGIN(cwp);
         int emitted = 0;
         while (!done && emitted < kDescPerWarp) {
             SIMBA_WD("plan", n, emitted);
@@ -1571,9 +1573,17 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                 have_piece = false;
             }
         }
+        SIMBA_CYC_END(p, ST_W_PLAN, cwp);
         if (lane == 0 && !done)
             atomicAdd(&ps->active, 1u);
         __syncthreads();
+#ifdef SIMBA_STATS
+        if (threadIdx.x == 0) {
+            atomicAdd(&p.stats[2 * ST_PH_PLAN], 1ull);
+            atomicAdd(&p.stats[2 * ST_PH_PLAN + 1], (unsigned long long)(clock64() - cph));
+        }
+        const long long cpe = clock64();
+#endif
         const unsigned int nq = ps->qn;
         if (nq == 0 && ps->active == 0)
             break;  // uniform: every warp is done and nothing is queued
@@ -1600,6 +1610,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
         __syncthreads();
         // ---- execute: all warps drain the queue variant by variant
         const TileDesc<W, E> *q = desc_queue<W, E>(p);
+        SIMBA_CYC_BEGIN(cwe);
         for (;;) {
             unsigned int idx = 0;
             if (lane == 0)
@@ -1610,7 +1621,15 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             SIMBA_WD("exec", idx, nq);
             exec_desc<W, E>(p, st, q + ps->order[idx], lane, ss.count);
         }
+        SIMBA_CYC_END(p, ST_W_EXEC, cwe);
         __syncthreads();
+#ifdef SIMBA_STATS
+        if (threadIdx.x == 0) {
+            atomicAdd(&p.stats[2 * ST_PH_EXEC], 1ull);
+            atomicAdd(&p.stats[2 * ST_PH_EXEC + 1], (unsigned long long)(clock64() - cpe));
+        }
+        const long long cpv = clock64();
+#endif
         // ---- verify the deferred candidates with every thread of the CTA
         {
             const unsigned int nv = min(ps->vqn, p.vqcap);
@@ -1623,6 +1642,12 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             }
         }
         __syncthreads();
+#ifdef SIMBA_STATS
+        if (threadIdx.x == 0) {
+            atomicAdd(&p.stats[2 * ST_PH_VERIFY], (unsigned long long)nq);
+            atomicAdd(&p.stats[2 * ST_PH_VERIFY + 1], (unsigned long long)(clock64() - cpv));
+        }
+#endif
         if (threadIdx.x == 0)
             ps->vqn = 0;
         if (threadIdx.x == 0) {
@@ -2018,8 +2043,6 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     const uint64_t owned = (rq.shard < nsuper) ? (nsuper - rq.shard + rq.nshards - 1) / rq.nshards : 0;
     KParams p{};
     p.tabs = c->d_tabs;
-    p.tbl = c->d_blob;
-    p.tbl_len = c->tbl_len;
     p.gtbl = c->d_gtbl;
     p.gtbl_len = c->gtbl_len;
     p.RG = c->RG;

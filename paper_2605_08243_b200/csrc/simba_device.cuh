@@ -21,7 +21,10 @@ constexpr unsigned FULL = 0xffffffffu;
 enum : int {
     ST_RF_FOLD = 0, ST_RF_GEN, ST_RF_ROW, ST_CF_FOLD, ST_CF_GEN,
     ST_CYC_OUTER, ST_CYC_X, ST_CYC_TILE,  // (calls, SM cycles) of the odometer steps and tile calls
-    ST_DIRECT, ST_N
+    ST_DIRECT,
+    ST_PH_PLAN, ST_PH_EXEC, ST_PH_VERIFY,  // (phases, CTA cycles) of each phase (thread 0)
+    ST_W_PLAN, ST_W_EXEC,                 // (warp phases, warp busy cycles) inside plan / exec
+    ST_N
 };
 #ifdef SIMBA_STATS
 #define SIMBA_STAT(p, i, cands)                                                         \
@@ -65,11 +68,7 @@ struct __align__(16) Tabs {
 
 struct KParams {
     const Tabs *tabs;        // global copy of the tables
-    const void *tbl;         // unused (kept for layout); see gtbl / shared copy
     const void *gtbl;        // [E][gtbl_len] values of every subtree of size <= RG (global)
-    const uint64_t *X;       // [n][k] inputs
-    const uint64_t *Y;       // [n] outputs
-    uint32_t tbl_len;        // entries of sizes <= R0 (shared-memory copy, example 0)
     uint32_t gtbl_len;       // entries of sizes <= RG per example (global)
     int k, n, s, R0, RG, E;
     int mode;                // SIMBA_MODE_*

@@ -265,7 +265,8 @@ class DeviceContext:
         N.check_rc(N.lib.simba_ctx_stream(self._ptr, C.byref(h)))
         return h.value or 0
 
-    PATHS = ("rf_fold", "rf_gen", "rf_row", "cf_fold", "cf_gen", "cyc_outer", "cyc_x", "cyc_tile", "direct")
+    PATHS = ("rf_fold", "rf_gen", "rf_row", "cf_fold", "cf_gen", "cyc_outer", "cyc_x", "cyc_tile", "direct",
+             "ph_plan", "ph_exec", "ph_verify", "w_plan", "w_exec")
 
     def path_stats(self) -> dict:
         """Per-path (calls, candidates) of the unit kernel since creation;

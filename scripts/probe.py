@@ -22,8 +22,12 @@ def run(label, spec, sizes, **kw):
             r = ctx.count(s)
             st = ctx.path_stats()
             if st:
-                cyc = {k: v for k, v in st.items() if k.startswith("cyc")}
-                paths = {k: v for k, v in st.items() if not k.startswith("cyc")}
+                cyc = {k: v for k, v in st.items() if k.startswith(("cyc", "w_"))}
+                ph = {k: v for k, v in st.items() if k.startswith("ph_")}
+                paths = {k: v for k, v in st.items() if not k.startswith(("cyc", "w_", "ph_"))}
+                ctas = info["grid_blocks"]
+                print("   phases per CTA:", {k: (round(v[0] / ctas, 1), round(v[1] / ctas / 1e6, 2)) for k, v in ph.items()},
+                      "Mcyc (ph_verify count = descriptors)")
                 tot = sum(v[1] for v in paths.values()) or 1
                 print("   paths:", {k: (v[0], round(100 * v[1] / tot, 2)) for k, v in paths.items() if v[0]})
                 warps = info["grid_blocks"] * info["block_threads"] // 32
