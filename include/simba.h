@@ -196,6 +196,45 @@ int simba_ctx_stats(simba_ctx *ctx, uint64_t *out, int n);
 
 const char *simba_last_error(void);
 int simba_device_count(void);
+/* ---------------------------------------------------------------------- */
+/* VFB cache-based baseline (baseline.run_baseline, baseline.py:88-249)     */
+/* ---------------------------------------------------------------------- */
+
+/* The paper's comparison point: bottom-up enumeration
+ * over cached behaviour vectors with observational-equivalence pruning.
+ * A run is one simba_vfb object; sizes are stepped in order 1, 2, ... by
+ * simba_vfb_level, which reports the per-size row of baseline.py's
+ * CacheSizeRow (baseline.py:51-58) and the event that ended the run. */
+typedef struct simba_vfb simba_vfb;
+
+#define SIMBA_VFB_NONE 0      /* the size ran to completion */
+#define SIMBA_VFB_FOUND 1     /* a candidate matched the outputs (baseline.py:156-158) */
+#define SIMBA_VFB_OOM 2       /* modeled storage exceeded the budget (baseline.py:161-163) */
+#define SIMBA_VFB_TIMED_OUT 3 /* the time budget expired between batches (baseline.py:149-153) */
+
+typedef struct {
+    uint64_t candidates;  /* candidates considered at this size (the ending one included) */
+    uint64_t stored;      /* entries newly stored at this size */
+    uint64_t stored_cum;  /* entries stored over all sizes */
+    uint64_t event_index; /* candidate index (in the size's order) of a FOUND / OOM event */
+    int32_t event;        /* SIMBA_VFB_* */
+    double millis;        /* host wall time of the size */
+} simba_vfb_row;
+
+/* inputs row-major [n][k], outputs [n] (validated by the caller as in
+ * Specification); max_entries = memory_budget / entry_bytes (UINT64_MAX when
+ * entries model 0 bytes).  Device memory grows with the entries stored;
+ * exhausting it is SIMBA_ENOMEM (not the modeled OOM). */
+int simba_vfb_create(int k, int w, int n, const uint64_t *inputs, const uint64_t *outputs, uint64_t max_entries,
+                     int device, simba_vfb **out);
+/* Runs one size (must be the previous size + 1).  time_budget_s < 0: none,
+ * else the size stops with SIMBA_VFB_TIMED_OUT once this many seconds have
+ * passed at a batch boundary. */
+int simba_vfb_level(simba_vfb *v, int size, double time_budget_s, simba_vfb_row *out);
+/* RPN tokens (expr.py:66-85) of candidate `cand` of the last size run. */
+int simba_vfb_tokens(simba_vfb *v, uint64_t cand, int32_t *tokens, int cap, int *len);
+void simba_vfb_destroy(simba_vfb *v);
+
 /* Kernels this library has launched in this process. */
 uint64_t simba_launch_count(void);
 

@@ -11,7 +11,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SRC = [PKG / "csrc" / "simba.cu"]
-DEPS = SRC + [PKG / "csrc" / "simba_device.cuh", ROOT / "include" / "simba.h"]
+DEPS = SRC + [PKG / "csrc" / "simba_device.cuh", PKG / "csrc" / "vfb_impl.cuh", ROOT / "include" / "simba.h"]
 OUT = PKG / "_lib" / "libsimba.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

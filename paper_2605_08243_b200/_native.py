@@ -90,6 +90,20 @@ class Outcome(C.Structure):
     ]
 
 
+VFB_NONE, VFB_FOUND, VFB_OOM, VFB_TIMED_OUT = 0, 1, 2, 3
+
+
+class VfbRow(C.Structure):
+    _fields_ = [
+        ("candidates", C.c_uint64),
+        ("stored", C.c_uint64),
+        ("stored_cum", C.c_uint64),
+        ("event_index", C.c_uint64),
+        ("event", C.c_int32),
+        ("millis", C.c_double),
+    ]
+
+
 # every symbol include/simba.h declares, with its ctypes signature
 SIGNATURES = {
     "simba_table_build": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
@@ -110,6 +124,11 @@ SIGNATURES = {
     "simba_ctx_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "simba_ctx_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int]),
     "simba_int32_peak": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "simba_vfb_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                   C.c_uint64, C.c_int, C.POINTER(C.c_void_p)]),
+    "simba_vfb_level": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.POINTER(VfbRow)]),
+    "simba_vfb_tokens": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32), C.c_int, C.POINTER(C.c_int)]),
+    "simba_vfb_destroy": (None, [C.c_void_p]),
     "simba_last_error": (C.c_char_p, []),
     "simba_device_count": (C.c_int, []),
     "simba_launch_count": (C.c_uint64, []),

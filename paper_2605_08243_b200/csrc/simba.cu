@@ -2870,3 +2870,5 @@ int simba_decode(simba_ctx *c, uint64_t rank, int size, int32_t *tokens)
 }
 
 }  // extern "C"
+
+#include "vfb_impl.cuh"

@@ -8,7 +8,7 @@ Test infrastructure only; run in the build container:
 Writes tests/golden/suite.json with
   suite      bench.generate_suite(seed, sizes, vars, per_cell) written by
              bench.write_suite (the exact JSONL text)            [bench.py:90-137, 172-194]
-  records    bench.run_suite(suite, solvers=("simba", "simba-rtid"), timeout=None)
+  records    bench.run_suite(suite, solvers=("simba", "simba-rtid", "baseline"), timeout=None)
              statuses/sizes per instance and the normalized labels [bench.py:234-304, 140-163]
   summary    bench.summarize on a fixed synthetic record set      [bench.py:340-440]
 """
@@ -34,7 +34,7 @@ def main():
         path = os.path.join(td, "suite.jsonl")
         bench.write_suite(path, suite, seed=SEED)
         text = Path(path).read_text()
-    records, normalized = bench.run_suite(suite, solvers=("simba", "simba-rtid"), timeout=None)
+    records, normalized = bench.run_suite(suite, solvers=("simba", "simba-rtid", "baseline"), timeout=None)
     rec = [{"instance": r.instance, "solver": r.solver, "status": r.status, "size": r.size} for r in records]
     norm = [{"id": i.id, "norm_size": i.norm_size, "norm_vars": i.norm_vars,
              "norm_upper_bound": i.norm_upper_bound} for i in normalized]

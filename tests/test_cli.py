@@ -76,3 +76,21 @@ def test_count_solutions_cli(capsys, tmp_path):
     code, out, _ = run(capsys, "count-solutions", "--spec", str(path), "--max-size", "3")
     doc = json.loads(out)
     assert code == 0 and doc[0]["count"] == 1 and doc[0]["first_rank"] == "0"
+
+
+@pytest.mark.gpu
+def test_baseline_subcommand(capsys, tmp_path):
+    """reference test_cli.py:145-152: the cache report, then the formula."""
+    path = identity_spec(tmp_path / "id.spec")
+    code, out, _ = run(capsys, "baseline", "--spec", str(path), "--max-size", "3")
+    assert code == 0
+    assert "#VFB cache" in out
+    assert "found: x0 (size 1)" in out
+    code, out, _ = run(capsys, "baseline", "--spec", str(path), "--max-size", "3", "--report", "csv")
+    assert code == 0 and out.startswith("Size,#MBA,#VFB cache")
+
+
+def test_baseline_usage(capsys):
+    with pytest.raises(SystemExit) as exc:
+        main(["baseline", "--max-size", "3"])
+    assert exc.value.code == EXIT_USAGE

@@ -68,7 +68,7 @@ def test_summaries_match_reference(tmp_path):
 def test_bench_cli_rejects_unknown_solver(tmp_path, capsys):
     p = tmp_path / "suite.jsonl"
     p.write_text(GOLD["suite_jsonl"])
-    rc = cli.main(["bench", "run", "--suite", str(p), "--solvers", "baseline", "--records", str(tmp_path / "r.csv")])
+    rc = cli.main(["bench", "run", "--suite", str(p), "--solvers", "vfb", "--records", str(tmp_path / "r.csv")])
     assert rc == cli.EXIT_IO
 
 
@@ -86,7 +86,7 @@ def test_generate_suite_matches_reference(tmp_path):
 @pytest.mark.gpu
 def test_run_suite_matches_reference(tmp_path):
     items = _suite_from_text(tmp_path)
-    records, normalized = suite.run_suite(items, solvers=("simba", "simba-rtid"), timeout=None)
+    records, normalized = suite.run_suite(items, solvers=("simba", "simba-rtid", "baseline"), timeout=None)
     assert [{"instance": r.instance, "solver": r.solver, "status": r.status, "size": r.size}
             for r in records] == GOLD["records"]
     assert [{"id": i.id, "norm_size": i.norm_size, "norm_vars": i.norm_vars,
@@ -98,9 +98,9 @@ def test_bench_cli_end_to_end(tmp_path):
     p = tmp_path / "suite.jsonl"
     assert cli.main(["bench", "gen", "--seed", str(GOLD["seed"]), "--out", str(p), "--sizes", "3..4",
                      "--vars", "2", "--per-cell", "2"]) == 0
-    rc = cli.main(["bench", "run", "--suite", str(p), "--solvers", "simba,simba-rtid",
+    rc = cli.main(["bench", "run", "--suite", str(p), "--solvers", "simba,simba-rtid,baseline", "--timeout", "30",
                    "--records", str(tmp_path / "r.csv"), "--summary-dir", str(tmp_path / "sum")])
     assert rc == 0
     recs = suite.read_records_csv(tmp_path / "r.csv")
-    assert len(recs) == 8 and all(r.status == "found" for r in recs)
+    assert len(recs) == 12 and all(r.status == "found" for r in recs)
     assert sorted(x.name for x in (tmp_path / "sum").iterdir()) == sorted(GOLD["summary_csvs"])
