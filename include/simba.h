@@ -171,6 +171,11 @@ int simba_synthesize(simba_ctx *ctx, int size_bound, int shuffled, double time_b
 /* codec.decode(rank, size, table) (codec.py:136-144) on the device. */
 int simba_decode(simba_ctx *ctx, uint64_t rank, int size, int32_t *tokens);
 
+/* Decode of the ranks [rank0, rank0 + count) of one size into
+ * tokens[count][size] (one thread per rank): the sweep of
+ * engine.enumerate_all (engine.py:279-293). */
+int simba_decode_batch(simba_ctx *ctx, uint64_t rank0, uint64_t count, int size, int32_t *tokens);
+
 /* Effective configuration of a context (for reports): r0, rg, table
  * examples, word bytes, grid blocks, block threads, shared-memory bytes per block. */
 int simba_ctx_info(simba_ctx *ctx, int *r0, int *rg, int *table_examples, int *word_bytes, int *grid_blocks,

@@ -119,6 +119,7 @@ SIGNATURES = {
                                    C.POINTER(Level), C.POINTER(Result)]),
     "simba_synthesize": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_double, C.POINTER(Outcome)]),
     "simba_decode": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
+    "simba_decode_batch": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
     "simba_ctx_info": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int)] * 7),
     "simba_ctx_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "simba_ctx_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

@@ -1748,6 +1748,18 @@ __global__ void decode_kernel(const Tabs *tabs, uint64_t rank, int size, int32_t
         out[i] = buf[i];
 }
 
+// decode of `count` consecutive ranks from rank0 (enumerate_all, engine.py:279-293)
+__global__ void decode_batch_kernel(const Tabs *tabs, uint64_t rank0, uint64_t count, int size, int32_t *out)
+{
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        int8_t buf[MAXS];
+        decode_tokens(tabs, rank0 + i, size, buf);
+        for (int j = 0; j < size; ++j)
+            out[i * size + j] = buf[j];
+    }
+}
+
 }  // namespace simba
 
 // ===========================================================================
@@ -2854,6 +2866,33 @@ int simba_ctx_stats(simba_ctx *c, uint64_t *out, int n)
     (void)n;
     return 0;
 #endif
+}
+
+int simba_decode_batch(simba_ctx *c, uint64_t rank0, uint64_t count, int size, int32_t *tokens)
+{
+    if (!c || (!tokens && count))
+        return fail(SIMBA_EINVAL, "null argument");
+    if (size < 1 || size > c->max_size)
+        return fail(SIMBA_ERANGE, "size %d outside table extent 1..%d", size, c->max_size);
+    const uint64_t total = row_total(c, size);
+    if (rank0 > total || count > total - rank0)
+        return fail(SIMBA_ERANGE, "ranks [%llu, %llu + %llu) out of range for size %d (total %llu)",
+                    (unsigned long long)rank0, (unsigned long long)rank0, (unsigned long long)count, size,
+                    (unsigned long long)total);
+    if (count == 0)
+        return SIMBA_OK;
+    CK(cudaSetDevice(c->device));
+    const uint64_t bytes = count * (uint64_t)size * sizeof(int32_t);
+    int32_t *d = nullptr;
+    CK(cudaMallocAsync(&d, bytes, c->stream));
+    const uint64_t blocks = std::min<uint64_t>((count + 255) / 256, 148ull * 32);
+    decode_batch_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(c->d_tabs, rank0, count, size, d);
+    g_launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(tokens, d, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaFreeAsync(d, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SIMBA_OK;
 }
 
 int simba_decode(simba_ctx *c, uint64_t rank, int size, int32_t *tokens)

@@ -282,6 +282,15 @@ class DeviceContext:
         N.check_rc(N.lib.simba_decode(self._ptr, rank, size, buf))
         return tuple(buf[:size])
 
+    def decode_batch(self, rank0: int, count: int, size: int):
+        """Tokens of the ranks [rank0, rank0 + count), as a (count, size) int32 array."""
+        import numpy as np
+
+        out = np.empty((count, size), dtype=np.int32)
+        N.check_rc(N.lib.simba_decode_batch(self._ptr, rank0, count, size,
+                                            out.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out
+
     def total(self, size: int) -> int:
         return self.table.total(size)
 
@@ -331,6 +340,22 @@ def count_solutions(spec: Specification, table: CountTable, cfg: EngineConfig) -
             tot = sum(v for *_, v in levels) or 1
             out = [SizeCount(s, c, f, v, ms * v / tot) for s, c, f, v in levels]
     return tuple(out)
+
+
+def enumerate_all(size: int, table: CountTable, visitor=None, batch: int = 1 << 20) -> int:
+    """engine.enumerate_all (engine.py:279-293): decode every rank of ``size``
+    once (on the device, in batches) and hand each expression to ``visitor``
+    in rank order; returns the number of ranks."""
+    from .codec import _decoder
+
+    total = table.total(size)
+    dec = _decoder(table)
+    for r0 in range(0, total, batch):
+        toks = dec.decode_batch(r0, min(batch, total - r0), size)
+        if visitor is not None:
+            for row in toks.tolist():
+                visitor(RpnExpr(tuple(row)))
+    return total
 
 
 def run_stats(outcome: SynthesisOutcome) -> dict:

@@ -149,6 +149,11 @@ def check(expr: RpnExpr, spec) -> bool:
     return True
 
 
+def observational_behavior(expr: RpnExpr, spec) -> tuple[int, ...]:
+    """The outputs (e(x_1), ..., e(x_n)) in specification order (expr.py:221-229)."""
+    return tuple(evaluate(expr, inputs, spec.w) for inputs, _ in spec.pairs)
+
+
 def to_infix(expr: RpnExpr) -> str:
     """Fully parenthesised infix, identical text to expr.py:242-259."""
     stack: list[str] = []

@@ -265,3 +265,29 @@ def test_shuffled_scan_on_block_beyond_2_32():
                                 threads=O.cpu_count())
             got = ctx.scan_range(13, off, cnt, a, b, shuffled=True)
             assert got == (want[0], want[2], want[3]), a
+
+
+@pytest.mark.gpu
+def test_enumerate_all_and_sampling():
+    """engine.enumerate_all (engine.py:279-293) visits the device decode of
+    every rank in order; sample_uniform / decode / encode round trips
+    (test_engine.py:162-176, test_codec.py:156-183)."""
+    import random
+
+    import oracle as O
+    from paper_2605_08243_b200.codec import encode
+
+    assert S.enumerate_all(3, S.build(2, 3)) == 32
+    assert S.enumerate_all(1, S.build(5, 1)) == 5
+    for k, s in ((2, 5), (3, 4), (1, 7)):
+        tab, otab = S.build(k, s), O.OracleTable(k, s)
+        seen = []
+        assert S.enumerate_all(s, tab, lambda e: seen.append(e.tokens), batch=97) == tab.total(s)
+        assert seen == [tuple(O.decode(otab, n, s)) for n in range(tab.total(s))]
+    rng = random.Random(11)
+    tab = S.build(5, 12)
+    for s in range(1, 13):
+        e = S.sample_uniform(s, tab, rng)
+        assert e.size == s
+        r = encode(e, tab)
+        assert S.decode(r.value, s, tab) == e

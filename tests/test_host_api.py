@@ -146,3 +146,52 @@ def test_context_argument_errors_before_device():
     big_k = S.Specification.of([((0,) * 65, 0)], k=65)
     with pytest.raises(ValueError):
         S.DeviceContext(big_k, 3)
+
+
+def test_encode_examples_and_errors():
+    """codec.encode (codec.py:147-207): reference known answers
+    (test_codec.py:52-70)."""
+    from paper_2605_08243_b200.codec import CanonicalityError, Rank, encode
+
+    t2 = S.build(2, 5)
+    assert encode(parse_infix("(x0 & x1)", 2), t2) == Rank(5, 3)
+    assert encode(parse_infix("(x1 & x0)", 2), t2) == Rank(6, 3)
+    t3 = S.build(3, 5)
+    with pytest.raises(CanonicalityError):
+        encode(RpnExpr((0, 1, -2, 2, -2)), t3)  # (x0 & x1) & x2: left size 3 > right size 1
+    ok = RpnExpr((0, 1, -2, 2, -7))  # (x0 & x1) - x2: SUB takes any split
+    assert encode(ok, t3).size == 5
+    with pytest.raises(ValueError):
+        encode(RpnExpr((0, 1, -2)), S.build(1, 3))
+
+
+def test_encode_inverts_the_oracle_decode():
+    """Every rank at small (k, s), and sampled ranks at size 10, through the
+    CPU oracle's decode (oracle/simba_oracle.c, pinned to the reference)."""
+    import random
+
+    import oracle as O
+    from paper_2605_08243_b200.codec import encode
+
+    for k, smax in ((1, 7), (2, 6), (3, 5)):
+        tab, otab = S.build(k, smax), O.OracleTable(k, smax)
+        for s in range(1, smax + 1):
+            for n in range(tab.total(s)):
+                assert encode(RpnExpr(O.decode(otab, n, s)), tab) == (n, s)
+    rng = random.Random(7)
+    tab, otab = S.build(4, 10), O.OracleTable(4, 10)
+    for _ in range(300):
+        n = rng.randrange(tab.total(10))
+        assert encode(RpnExpr(O.decode(otab, n, 10)), tab) == (n, 10)
+
+
+def test_observational_behavior():
+    spec = S.Specification.of([((3, 5), 8), ((7, 9), 16)], k=2)
+    assert S.observational_behavior(parse_infix("x0 + x1", 2), spec) == (8, 16)
+
+
+def test_cli_encode(capsys):
+    from paper_2605_08243_b200.cli import main
+
+    assert main(["encode", "--k", "2", "--expr", "(x0 & x1)"]) == 0
+    assert capsys.readouterr().out.split() == ["3", "5"]
