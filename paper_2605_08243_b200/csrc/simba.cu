@@ -86,7 +86,7 @@ constexpr int kCtrWords = 8;  // ctr, best, count, visited, units[2], flags, spa
 constexpr int kLvlWords = 3 * (SIMBA_MAX_SIZE + 1);  // per-level count, visited, first rank
 constexpr uint64_t kFuseCands = 1ull << 26;          // synthesize: levels fused per launch up to this many candidates
 constexpr uint64_t kSmemMax = 232448;  // opt-in dynamic shared memory per block (sm_100)
-constexpr uint64_t kTblPad = 256;      // words after the shared value table (8 x 32-lane reads)
+constexpr uint64_t kTblPad = 256;      // words after the global value table (8 x 32-lane reads past a row)
 
 }  // namespace
 
@@ -407,6 +407,10 @@ struct SweepStats {
 // predicate (no candidate is skipped or grouped by value).
 
 constexpr uint32_t kRFMin = 128;  // RF tiles for rows of at least this many columns
+#ifndef SIMBA_RF2D
+#define SIMBA_RF2D 1024
+#endif
+constexpr uint32_t kRF2D = SIMBA_RF2D;  // rows of at least this many columns: 2-D (rows x column chunk) tiles
 #ifndef SIMBA_CFSHORT
 #define SIMBA_CFSHORT 128
 #endif
@@ -827,7 +831,7 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
     Seg<W> *buf = L->tbuf;
     const TileArgs<W> &ta = L->tac;
     const Seg<W> (&sl)[MAXSL] = L->sl0;
-    const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));
+    const W *t0 = reinterpret_cast<const W *>(p.gtbl);  // column values: example 0 of the global table
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);
     TPair<W> *pb = reinterpret_cast<TPair<W> *>(buf);
     const W TM = ta.tm, TC = ta.tc;
@@ -936,7 +940,7 @@ __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int p
     WarpLevels<W, E> *L = reinterpret_cast<WarpLevels<W, E> *>(smem + p.lvl_off) + (threadIdx.x >> 5);
     const SegStash<W, E> *sx = &L->stash;
     const TileArgs<W> &ta = L->tac;
-    const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));
+    const W *t0 = reinterpret_cast<const W *>(p.gtbl);  // column values: example 0 of the global table
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);
     W m = ta.tm, c = ta.tc;
     if (pop != OP_NONE) {
@@ -948,11 +952,18 @@ __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int p
         rows_left<W, 1>(g0, xu, row0, 1, lane, slr, xr);
         fold_p(pop, xr[0], true, ta.tm, ta.tc, m, c);
     }
+    // column values come from L2: the next 256-column chunk is loaded while
+    // this one is tested
+    W s[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        s[j] = __ldg(t0 + off2 + clo + lane + 32 * j);
     for (uint32_t c0 = clo; c0 < chi; c0 += 256) {
-        W s[8];
+        W sn[8];
+        const uint32_t cn = (c0 + 256 < chi) ? c0 + 256 : c0;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-            s[j] = t0[off2 + c0 + lane + 32 * j];
+            sn[j] = __ldg(t0 + off2 + cn + lane + 32 * j);
         if (__any_sync(FULL, hit8(s, m, c))) {
             uint32_t bits = hitmask8(s, m, c);
             while (__any_sync(FULL, bits != 0)) {
@@ -963,6 +974,9 @@ __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int p
                 on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0, d2, my_count);
             }
         }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            s[j] = sn[j];
     }
     __syncwarp();
 }
@@ -981,7 +995,7 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop
     Seg<W> *buf = L->tbuf;
     const TileArgs<W> &ta = L->tac;
     const Seg<W> (&sl)[MAXSL] = L->sl0;
-    const W *t0 = reinterpret_cast<const W *>(smem + sizeof(Tabs));
+    const W *t0 = reinterpret_cast<const W *>(p.gtbl);  // column values: example 0 of the global table
     const W *g0 = reinterpret_cast<const W *>(p.gtbl);
     TPair<W> *pb = reinterpret_cast<TPair<W> *>(buf);
     const W TM = ta.tm, TC = ta.tc;
@@ -1365,9 +1379,31 @@ __device__ __forceinline__ uint64_t plan_pblock(const KParams &p, const Staged &
                 const uint64_t rs = d1 * R2;
                 const uint32_t clo = (uint32_t)(u - rs);
                 if (clo != 0 || u1 - rs < R2) {
-                    const uint32_t chi = (uint32_t)min((uint64_t)R2, u1 - rs);
+                    const uint32_t chi =
+                        (uint32_t)min(min((uint64_t)R2, u1 - rs), (uint64_t)clo + kDescCands);
                     emit_tile<W, E>(p, od, 0, pop, nt, xu, ubase, R2, off2, d1, 1, clo, chi, lane, emitted);
                     u = rs + chi;
+                } else if (pop != OP_NONE && R2 >= kRF2D) {
+                    // long rows: up to TILE_BUF rows x column chunks of ~kDescCands
+                    // candidates, so the rows' (m, c) and each column chunk are reused
+                    // across the whole block; a full queue resumes mid-group
+                    const uint64_t nf = min(div_T(t, prsz, u1 - u), (uint64_t)TILE_BUF);
+                    const uint32_t cw = (uint32_t)max((uint64_t)256, (uint64_t)(((kDescCands / nf) + 255) & ~255ull));
+                    uint32_t cc = 0;
+                    if (od.rs_valid && od.rs_n == ubase + u)
+                        cc = od.rs_c;
+                    od.rs_valid = false;
+                    for (; cc < R2; cc += cw) {
+                        if (emitted >= cap) {
+                            od.rs_valid = true;
+                            od.rs_n = ubase + u;
+                            od.rs_c = cc;
+                            return ubase + u;
+                        }
+                        emit_tile<W, E>(p, od, 0, pop, nt, xu, ubase, R2, off2, d1, nf, cc, min(cc + cw, R2), lane,
+                                        emitted);
+                    }
+                    u += nf * R2;
                 } else {
                     const uint64_t nf = min(div_T(t, prsz, u1 - u), rmax);
                     emit_tile<W, E>(p, od, (pop == OP_NONE || R2 >= kRFMin) ? 0 : 1, pop, nt, xu, ubase, R2, off2, d1,
@@ -1488,7 +1524,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     od.gt_e = reinterpret_cast<const W *>(p.gtbl) + (size_t)(lane & (E - 1)) * p.gtbl_len;
     od.RG = p.RG;
     od.s = p.s_lo;  // the level is (re)set per piece below
-    od.R0 = min(p.R0, od.s);
+    od.R0 = min(od.s >= p.r0_up ? p.R0 + 1 : p.R0, od.s);
     od.lane = lane;
     od.ex = lane & (E - 1);
     const bool early = (p.mode == SIMBA_MODE_SEARCH);
@@ -1548,7 +1584,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             const int s = level_of(p, n);
             if (s != od.s) {
                 od.s = s;
-                od.R0 = min(p.R0, s);
+                od.R0 = min(s >= p.r0_up ? p.R0 + 1 : p.R0, s);
                 od.reset();
             }
             const uint64_t vb = p.vbase[s];
@@ -1877,6 +1913,7 @@ void pool_put(int device, void *p, size_t bytes, bool host)
 struct simba_ctx {
     int device = 0, k = 0, w = 0, n = 0, max_size = 0;
     int wbytes = 4, R0 = 1, RG = 1, E = 1, kernel = 0;
+    int r0_up = MAXS + 1;  // first level whose units use R0 + 1
     uint32_t tbl_len = 0, gtbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
     unsigned char *d_gtbl = nullptr;
     int block_threads = 256, grid_unit = 0, grid_direct = 0;
@@ -1939,9 +1976,6 @@ int build_value_tables(simba_ctx *c)
         reinterpret_cast<W *>(c->d_gtbl));
     g_launches++;
     CK(cudaGetLastError());
-    // shared-memory copy: example 0, sizes <= R0 (a prefix of the global table)
-    CK(cudaMemcpyAsync(c->d_blob, c->d_gtbl, (size_t)c->tbl_len * sizeof(W), cudaMemcpyDeviceToDevice,
-                       c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return SIMBA_OK;
 }
@@ -2061,7 +2095,8 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.k = c->k;
     p.n = c->n;
     p.s = rq.size;
-    p.R0 = c->R0;  // min(R0, s) per level in the kernel
+    p.R0 = c->R0;  // min(R0 (+1 from level r0_up), s) per level in the kernel
+    p.r0_up = c->r0_up;
     p.s_lo = s_lo;
     p.s_hi = rq.size;
     p.vbase = c->d_lvl + kLvlWords;  // the level bases follow the per-level counters
@@ -2332,33 +2367,15 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         return r0;
     };
     const int full_warps = SIMBA_UNIT_THREADS / 32;
-    const int req_warps = o.block_threads ? o.block_threads / 32 : 0;
-    int warps_hint = 0;  // 0: the default choice below
     int R0 = o.r0;
     if (R0 == 0) {
-        // largest shared-memory table up to 160 KB: longer rows and fewer
-        // units beat a second CTA per SM (occupancy is register-bound anyway);
-        // when a 12-warp CTA admits a larger table than a 16-warp one
-        // (wide words, several table examples) it wins
-        R0 = largest_r0(table_cap(req_warps ? req_warps : full_warps));
-        if (!req_warps) {
-            const int r12 = largest_r0(table_cap(full_warps * 3 / 4));
-            if (r12 > R0) {
-                R0 = r12;
-                warps_hint = full_warps * 3 / 4;
-            }
-        }
+        // column tables of up to ~160 KB per size class (the measured optimum
+        // of rows x columns per unit for levels up to ~1e10 candidates; the
+        // largest levels step up one size below)
+        R0 = std::max(largest_r0(table_cap(full_warps)), largest_r0(table_cap(full_warps * 3 / 4)));
     } else {
         if (R0 < 1 || R0 > max_size)
             return bail(fail(SIMBA_EINVAL, "r0 %d outside 1..%d", R0, max_size));
-        for (int r = 1; r <= R0; ++r)
-            if (t.T[r] > 65535)
-                return bail(fail(SIMBA_EINVAL, "r0 %d: T[%d] exceeds 65535", R0, r));
-        if ((tbl_size(R0) + kTblPad) * c->wbytes > table_cap(req_warps ? req_warps : full_warps)) {
-            if (req_warps || (tbl_size(R0) + kTblPad) * c->wbytes > table_cap(full_warps * 3 / 4))
-                return bail(fail(SIMBA_EINVAL, "r0 %d: value table exceeds shared memory", R0));
-            warps_hint = full_warps * 3 / 4;
-        }
     }
     int RG = o.rg;
     if (RG == 0) {
@@ -2379,6 +2396,20 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     }
     c->R0 = R0;
     c->RG = RG;
+    // levels with at least T[R0+1] * 2^18 candidates use R0 + 1 (rows of
+    // T[R0+1] columns; fewer, larger units where the level is large enough
+    // that its claims still span many rows)
+    c->r0_up = MAXS + 1;
+    if (o.r0 == 0 && R0 + 1 <= RG) {
+        const uint64_t need = t.T[R0 + 1] << 18;
+        for (int s = 1; s <= max_size; ++s)
+            if (t.T[s] >= need) {
+                c->r0_up = s;
+                break;
+            }
+    }
+    if (const char *e = getenv("SIMBA_R0_UP"))
+        c->r0_up = atoi(e);
     {
         uint32_t off = 0, soff = 0;
         for (int z = 1; z <= MAXS; ++z) {
@@ -2389,19 +2420,16 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
                 soff += (uint32_t)t.T[z];
         }
         c->gtbl_len = off;
-        c->tbl_len = soff;
+        c->tbl_len = 0;  // tiles read column values from the global table (L2-resident)
+        (void)soff;
     }
     auto pad16 = [](uint64_t b) { return (uint32_t)((b + 15) & ~15ull); };
-    c->tbl_bytes = pad16((uint64_t)(c->tbl_len + kTblPad) * c->wbytes);  // unrolled reads past a row
+    c->tbl_bytes = 0;  // no shared-memory value table
     c->ex_bytes = pad16((uint64_t)n * (k + 1) * c->wbytes);
     c->stage_examples = c->ex_bytes <= 32 * 1024;
     // 16 warps per SM either way (128 registers per thread): one 512-thread CTA
     // when the shared-memory tables do not leave room for two
-    c->block_threads = o.block_threads ? o.block_threads
-                       : warps_hint     ? warps_hint * 32
-                                        : ((sizeof(Tabs) + c->tbl_bytes + c->ex_bytes > 100 * 1024)
-                                               ? SIMBA_UNIT_THREADS
-                                               : (SIMBA_UNIT_THREADS > 256 ? SIMBA_UNIT_THREADS / 2 : 256));
+    c->block_threads = o.block_threads ? o.block_threads : SIMBA_UNIT_THREADS;
     if (c->block_threads % 32 || c->block_threads < 32 || c->block_threads > SIMBA_UNIT_THREADS)
         return bail(fail(SIMBA_EINVAL, "block_threads must be a multiple of 32 in 32..%d", SIMBA_UNIT_THREADS));
     c->lvl_off = (uint32_t)(sizeof(Tabs) + c->tbl_bytes + (c->stage_examples ? c->ex_bytes : 0));
@@ -2444,7 +2472,8 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
         const size_t o_blob = up(sizeof(Tabs));
         const size_t o_gtbl = up(o_blob + (size_t)c->tbl_bytes + c->ex_bytes);
-        const size_t o_ctr = up(o_gtbl + (size_t)c->E * c->gtbl_len * c->wbytes + 16);
+        // + kTblPad words: tiles read whole 256-column chunks past a row's end
+        const size_t o_ctr = up(o_gtbl + ((size_t)c->E * c->gtbl_len + kTblPad) * c->wbytes + 16);
         const size_t o_tok = up(o_ctr + sizeof(unsigned long long) * kCtrWords);
         const size_t o_stats = up(o_tok + sizeof(int32_t) * MAXS);
         const size_t o_queue = up(o_stats + sizeof(unsigned long long) * 2 * ST_N);

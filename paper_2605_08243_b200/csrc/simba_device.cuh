@@ -71,6 +71,7 @@ struct KParams {
     const void *gtbl;        // [E][gtbl_len] values of every subtree of size <= RG (global)
     uint32_t gtbl_len;       // entries of sizes <= RG per example (global)
     int k, n, s, R0, RG, E;
+    int r0_up;               // levels >= r0_up use R0 + 1
     int mode;                // SIMBA_MODE_*
     int shuffled;
     uint64_t mask;
@@ -559,6 +560,10 @@ struct Odometer {
     bool so0_bw;           // innermost outer segment has a bitwise part
     uint32_t gen;          // bumped whenever the outer chain (so) is recomposed
     bool ovf_o, ovf_l;
+    // planner resume point inside a 2-D row group (queue filled mid-group)
+    bool rs_valid;
+    uint32_t rs_c;
+    uint64_t rs_n;
 
     __device__ __forceinline__ void reset()
     {
@@ -566,6 +571,7 @@ struct Odometer {
         nx = 0;
         have_outer = false;
         have_x = false;
+        rs_valid = false;
     }
 
     __device__ __forceinline__ W sib_value(int j, uint64_t q) const

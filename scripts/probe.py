@@ -37,23 +37,24 @@ def run(label, spec, sizes, **kw):
                   f"{r.visited / (r.kernel_ms * 1e-3):.3e} cand/s cnt={r.count} units={r.units} "
                   f"rank_units={r.rank_units} ctx={tc*1e3:.0f}ms {info}", flush=True)
 
-spec4 = unsat(4, 32, 10, 31337)
-if len(sys.argv) > 1 and sys.argv[1] == "r0":
-    run("C5 r0=5 256x2", spec4, [11, 12, 13])
-    run("C5 r0=5 512x1", spec4, [11, 12, 13], block_threads=512)
-    run("C5 r0=6 512x1", spec4, [11, 12, 13], r0=6, block_threads=512)
-    run("C3 r0=6 256x2", unsat(3, 32, 10, 777), [11, 12])
-    run("C3 r0=7 512x1", unsat(3, 32, 10, 777), [11, 12], r0=7, block_threads=512)
-    sys.exit()
-if len(sys.argv) > 1:
-    run("C5 unit", spec4, [int(a) for a in sys.argv[1:]]); sys.exit()
-run("C5 unit", spec4, [9, 10, 11, 12, 13])
-run("C5 unit rg=8", spec4, [12, 13], rg=8)
-run("C5 direct", spec4, [9, 10], kernel="direct")
-run("C5 unit r0=4", spec4, [11], r0=4)
-spec3 = unsat(3, 32, 10, 777)
-run("C3 unit", spec3, [9, 10, 11, 12])
-spec4w = unsat(3, 64, 100, 4242)
-run("C4 unit", spec4w, [9, 10, 11])
-spec2 = unsat(2, 32, 10, 99)
-run("C2 unit", spec2, [7, 10, 13])
+if __name__ == "__main__":
+    spec4 = unsat(4, 32, 10, 31337)
+    if len(sys.argv) > 1 and sys.argv[1] == "r0":
+        run("C5 r0=5 256x2", spec4, [11, 12, 13])
+        run("C5 r0=5 512x1", spec4, [11, 12, 13], block_threads=512)
+        run("C5 r0=6 512x1", spec4, [11, 12, 13], r0=6, block_threads=512)
+        run("C3 r0=6 256x2", unsat(3, 32, 10, 777), [11, 12])
+        run("C3 r0=7 512x1", unsat(3, 32, 10, 777), [11, 12], r0=7, block_threads=512)
+        sys.exit()
+    if len(sys.argv) > 1:
+        run("C5 unit", spec4, [int(a) for a in sys.argv[1:]]); sys.exit()
+    run("C5 unit", spec4, [9, 10, 11, 12, 13])
+    run("C5 unit rg=8", spec4, [12, 13], rg=8)
+    run("C5 direct", spec4, [9, 10], kernel="direct")
+    run("C5 unit r0=4", spec4, [11], r0=4)
+    spec3 = unsat(3, 32, 10, 777)
+    run("C3 unit", spec3, [9, 10, 11, 12])
+    spec4w = unsat(3, 64, 100, 4242)
+    run("C4 unit", spec4w, [9, 10, 11])
+    spec2 = unsat(2, 32, 10, 99)
+    run("C2 unit", spec2, [7, 10, 13])
