@@ -82,10 +82,14 @@ int fail(int code, const char *fmt, ...)
     } while (0)
 
 constexpr uint64_t kShuffleMult = 2246822507ULL;  // codec.py:29
-constexpr int kCtrWords = 8;  // ctr, best, count, visited, units[2], flags, spare
+constexpr int kCtrWords = 8;  // ctr, best, count, visited, units[2], flags, planned
 constexpr int kLvlWords = 3 * (SIMBA_MAX_SIZE + 1);  // per-level count, visited, first rank
 constexpr uint64_t kFuseCands = 1ull << 26;          // synthesize: levels fused per launch up to this many candidates
 constexpr uint64_t kSmemMax = 232448;  // opt-in dynamic shared memory per block (sm_100)
+#ifndef SIMBA_R0_SHIFT
+#define SIMBA_R0_SHIFT 16  // a level uses R0 + 1 from T[R0+1] * 2^SHIFT candidates per shard and launch
+#endif
+constexpr uint32_t kPoolSlots = 1024;  // returned ranges (late splitting) per launch
 constexpr uint64_t kTblPad = 256;      // words after the global value table (8 x 32-lane reads past a row)
 
 }  // namespace
@@ -1154,15 +1158,21 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 #define SIMBA_DPW 24
 #endif
 #ifndef SIMBA_DESC_LOG2
-#define SIMBA_DESC_LOG2 17
+#define SIMBA_DESC_LOG2 18
 #endif
 constexpr int kDescPerWarp = SIMBA_DPW;
+#ifndef SIMBA_PHASE_GUIDE
+#define SIMBA_PHASE_GUIDE 0  // 0: no phase budget (measured best for single launches)
+#endif
+constexpr uint64_t kPhaseGuide = SIMBA_PHASE_GUIDE;  // phase budget ~ remaining / (warps * kPhaseGuide)
 constexpr uint32_t kVerifyCap = 8192;  // deferred verifications per CTA and phase
 #ifndef SIMBA_SUPER_PER_SHARD
 #define SIMBA_SUPER_PER_SHARD 16
 #endif
 constexpr uint64_t kSuperPerShard = SIMBA_SUPER_PER_SHARD;  // round-robin super-chunks per shard
-constexpr uint64_t kDescCands = 1ull << SIMBA_DESC_LOG2;  // candidates per descriptor (load balance)
+// candidates per descriptor (load balance): p.desc_cands, 2^SIMBA_DESC_LOG2 for
+// launches of at least kBigLaunch candidates, half that below
+constexpr uint64_t kDescCandsBig = 1ull << SIMBA_DESC_LOG2;
 constexpr int kVariants = 13;
 constexpr int kSizeClasses = 4;  // per variant, largest descriptors first (shorter phase tails)
 constexpr int kBuckets = kVariants * kSizeClasses;
@@ -1196,11 +1206,12 @@ __device__ __forceinline__ int variant_of(int kind, int nt, uint64_t nrows)
 }
 
 template <class W, int E>
-__device__ __forceinline__ void emit_tile(const KParams &p, const Odometer<W, E> &od, int kind, int pop, int nt,
+__device__ __forceinline__ void emit_tile(const KParams &p, Odometer<W, E> &od, int kind, int pop, int nt,
                                           const XU &xu, uint64_t ubase, uint32_t R2, uint32_t off2, uint64_t row0,
                                           uint64_t nrows, uint32_t clo, uint32_t chi, int lane, int &emitted)
 {
     PlanShared *ps = plan_shared(p);
+    const uint64_t cands = nrows * (uint64_t)(chi - clo);  // warp-uniform
     unsigned int slot = 0;
     if (lane == 0)
         slot = atomicAdd(&ps->qn, 1u);
@@ -1230,8 +1241,7 @@ __device__ __forceinline__ void emit_tile(const KParams &p, const Odometer<W, E>
         d->sz1 = (int8_t)xu.sz1;
         d->szy = (int8_t)xu.szy;
         d->s = od.s;
-        const uint64_t cands = nrows * (uint64_t)(chi - clo);
-        const int cls = cands >= (kDescCands >> 2) ? 0 : cands >= (kDescCands >> 5) ? 1 : cands >= 1024 ? 2 : 3;
+        const int cls = cands >= (p.desc_cands >> 2) ? 0 : cands >= (p.desc_cands >> 5) ? 1 : cands >= 1024 ? 2 : 3;
         ps->var[slot] = (uint8_t)(variant_of(kind, nt, nrows) * kSizeClasses + cls);
     }
     if constexpr (E > 1) {  // lane e holds example e's chains (hit refinement)
@@ -1245,6 +1255,11 @@ __device__ __forceinline__ void emit_tile(const KParams &p, const Odometer<W, E>
         }
     }
     ++emitted;
+    // the phase's candidate budget (shrinks with the launch's remaining work):
+    // once spent, the warp stops planning for this phase
+    od.phase_cands += cands;
+    if (od.phase_cands >= od.phase_budget)
+        emitted = max(emitted, kDescPerWarp);
 }
 
 // One descriptor: stage its chains in the warp's shared block, run the tile.
@@ -1367,11 +1382,12 @@ __device__ __forceinline__ uint64_t plan_pblock(const KParams &p, const Staged &
             direct_range<W>(p, st, n, stop, false, ss.count, od.s);
         } else {
             // unit-local candidates u = d1 * R2 + d2 in [u0, u1): full rows in
-            // RF (R2 >= kRFMin) or CF tiles of at most kDescCands candidates,
+            // RF (R2 >= kRFMin) or CF tiles of at most p.desc_cands candidates,
             // partial rows as one-row RF tiles; one descriptor each
             const uint64_t u1 = stop - ubase;
             uint64_t u = n - ubase;
-            const uint64_t rmax = max((uint64_t)1, (uint64_t)kDescCands / R2);
+            const uint64_t dc = p.desc_cands;
+            const uint64_t rmax = max((uint64_t)1, dc / R2);
             while (u < u1) {
                 if (emitted >= cap)
                     return ubase + u;  // queue full: resume here in the next phase
@@ -1380,15 +1396,15 @@ __device__ __forceinline__ uint64_t plan_pblock(const KParams &p, const Staged &
                 const uint32_t clo = (uint32_t)(u - rs);
                 if (clo != 0 || u1 - rs < R2) {
                     const uint32_t chi =
-                        (uint32_t)min(min((uint64_t)R2, u1 - rs), (uint64_t)clo + kDescCands);
+                        (uint32_t)min(min((uint64_t)R2, u1 - rs), (uint64_t)clo + dc);
                     emit_tile<W, E>(p, od, 0, pop, nt, xu, ubase, R2, off2, d1, 1, clo, chi, lane, emitted);
                     u = rs + chi;
                 } else if (pop != OP_NONE && R2 >= kRF2D) {
-                    // long rows: up to TILE_BUF rows x column chunks of ~kDescCands
+                    // long rows: up to TILE_BUF rows x column chunks of ~desc_cands
                     // candidates, so the rows' (m, c) and each column chunk are reused
                     // across the whole block; a full queue resumes mid-group
                     const uint64_t nf = min(div_T(t, prsz, u1 - u), (uint64_t)TILE_BUF);
-                    const uint32_t cw = (uint32_t)max((uint64_t)256, (uint64_t)(((kDescCands / nf) + 255) & ~255ull));
+                    const uint32_t cw = (uint32_t)max((uint64_t)256, (uint64_t)(((dc / nf) + 255) & ~255ull));
                     uint32_t cc = 0;
                     if (od.rs_valid && od.rs_n == ubase + u)
                         cc = od.rs_c;
@@ -1435,13 +1451,59 @@ struct Claim {
     uint64_t v0, v1;  // virtual chunk run [v0, v1)
 };
 
+// Late splitting.  Claims are sized in ranks, not in cost, so when the claim
+// counter runs dry some warps may still hold long stretches of expensive
+// ranks while others idle.  From then on a warp whose current piece has at
+// least kSplitMin ranks left hands the upper half to a global pool of ranges
+// (one split per phase); warps without work take ranges from the pool before
+// they finish.  A pusher always returns to the pool before exiting, so every
+// pushed range is taken.  Slot state: 0 empty, 1 full, 2/3 being written/read.
+#ifndef SIMBA_SPLIT_MIN_LOG2
+#define SIMBA_SPLIT_MIN_LOG2 19
+#endif
+constexpr uint64_t kSplitMin = SIMBA_SPLIT_MIN_LOG2 ? 1ull << SIMBA_SPLIT_MIN_LOG2 : 0;  // 0: no splitting
+
+__device__ __forceinline__ bool pool_push(const KParams &p, uint64_t a, uint64_t b, uint32_t start)
+{
+    for (uint32_t k = 0; k < kPoolSlots; ++k) {
+        unsigned long long *s = p.pool + 3 * ((start + k) % kPoolSlots);
+        if (atomicCAS(s, 0ull, 2ull) == 0ull) {
+            s[1] = a;
+            s[2] = b;
+            __threadfence();
+            atomicExch(s, 1ull);
+            return true;
+        }
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool pool_pop(const KParams &p, uint64_t &a, uint64_t &b, uint32_t start)
+{
+    for (uint32_t k = 0; k < kPoolSlots; ++k) {
+        unsigned long long *s = p.pool + 3 * ((start + k) % kPoolSlots);
+        if (*(volatile unsigned long long *)s == 1ull && atomicCAS(s, 1ull, 3ull) == 1ull) {
+            __threadfence();
+            a = *(volatile unsigned long long *)(s + 1);
+            b = *(volatile unsigned long long *)(s + 2);
+            atomicExch(s, 0ull);
+            return true;
+        }
+    }
+    return false;
+}
+
 #ifndef SIMBA_GUIDE
-#define SIMBA_GUIDE 8
+#define SIMBA_GUIDE 4
 #endif
 #ifndef SIMBA_CHUNK_LOG2
 #define SIMBA_CHUNK_LOG2 16  // small last claims: short launch tails (multi-GPU shards)
 #endif
-constexpr uint64_t kGuide = SIMBA_GUIDE;  // claim ~ remaining / (warps * kGuide)
+// claim ~ remaining / (warps * p.guide): SIMBA_GUIDE for launches of at least
+// kBigLaunch candidates (fewer, longer claims: fewer rows cut at claim
+// boundaries), twice that below (shorter tails when the launch is short)
+constexpr uint32_t kGuideBig = SIMBA_GUIDE;
+constexpr uint64_t kBigLaunch = 40000000000ull;
 
 __device__ __forceinline__ bool claim_run(const KParams &p, uint64_t t0, uint64_t &hint, Claim &cl)
 {
@@ -1457,7 +1519,7 @@ __device__ __forceinline__ bool claim_run(const KParams &p, uint64_t t0, uint64_
             cl.v0 = c;
             cl.v1 = min((uint64_t)(c + want), p.nvirt);
             const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-            hint = (p.nvirt - cl.v1) / (warps * kGuide);
+            hint = (p.nvirt - cl.v1) / (warps * p.guide);
             if (hint < 1)
                 hint = 1;
             // the time budget is polled between runs only and never masks a
@@ -1531,7 +1593,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     const uint64_t t0 = globaltimer_ns();
     SweepStats ss{0, 0, 0};
     uint64_t vis = 0;
-    uint64_t hint = p.nvirt / ((uint64_t)gridDim.x * (blockDim.x >> 5) * kGuide);
+    uint64_t hint = p.nvirt / ((uint64_t)gridDim.x * (blockDim.x >> 5) * p.guide);
     if (hint < 1)
         hint = 1;
     PlanShared *ps = plan_shared(p);
@@ -1550,18 +1612,74 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     Claim cl;
     bool have_claim = false, have_piece = false, done = false;
     uint64_t v = 0, c0 = 0, c1 = 0, n = 0;  // virtual ranks
+#ifdef SIMBA_CTA_TIMES
+    unsigned int nphase = 0;
+    __shared__ unsigned long long cta_dry;  // first time a warp of this CTA found no claim
+    if (threadIdx.x == 0)
+        cta_dry = ~0ull;
+    __syncthreads();
+#endif
     for (;;) {
+#ifdef SIMBA_CTA_TIMES
+        ++nphase;
+#endif
         // ---- plan: advance the odometer, queue up to kDescPerWarp tiles
         SIMBA_WD("phase", n, c1);
         SIMBA_CYC_BEGIN(cph);
         SIMBA_CYC_BEGIN(cwp);
         int emitted = 0;
+        {
+            // candidates this warp may plan in this phase: ~remaining / (warps x
+            // kPhaseGuide), so that late phases are short and CTAs finish together
+            unsigned long long planned = 0;
+            if (lane == 0)
+                planned = *(volatile unsigned long long *)p.planned;
+            planned = __shfl_sync(FULL, planned, 0);
+            const uint64_t all = p.nvirt * p.chunk_len;
+            const uint64_t rem = all - min((uint64_t)planned, all);
+            od.phase_budget = kPhaseGuide == 0 ? ~0ull
+                                               : max(p.desc_cands, rem / ((uint64_t)gridDim.x * (blockDim.x >> 5) *
+                                                                          (kPhaseGuide ? kPhaseGuide : 1)));
+            od.phase_cands = 0;
+        }
+        const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        if (kSplitMin && !done && have_piece && c1 - n >= kSplitMin) {
+            // claims ran dry: hand the upper half of this piece to the pool
+            int pushed = 0;
+            if (lane == 0 && *(volatile unsigned long long *)p.ctr >= p.nvirt) {
+                const uint64_t mid = n + (c1 - n) / 2;
+                pushed = pool_push(p, mid, c1, gw * 7u) ? 1 : 0;
+            }
+            if (__shfl_sync(FULL, pushed, 0))
+                c1 = n + (c1 - n) / 2;
+        }
         while (!done && emitted < kDescPerWarp) {
             SIMBA_WD("plan", n, emitted);
             if (!have_piece) {
                 if (!have_claim || v >= cl.v1) {
-                    if (!claim_run(p, t0, hint, cl)) {
+                    // claims first, then ranges other warps returned to the pool
+                    uint64_t pa = 0, pb = 0;
+                    int got = claim_run(p, t0, hint, cl) ? 1 : 0;
+                    if (!got && lane == 0)
+                        got = pool_pop(p, pa, pb, gw * 7u) ? 2 : 0;
+                    got = __shfl_sync(FULL, got, 0);
+                    if (got == 2) {
+                        c0 = __shfl_sync(FULL, pa, 0);
+                        c1 = __shfl_sync(FULL, pb, 0);
+                        have_claim = false;
+                        if (early && c0 > read_best(p))
+                            continue;  // ranks above a hit
+                        od.reset();
+                        n = c0;
+                        have_piece = true;
+                        continue;
+                    }
+                    if (!got) {
                         done = true;
+#ifdef SIMBA_CTA_TIMES
+                        if (lane == 0)
+                            atomicMin(&cta_dry, (unsigned long long)globaltimer_ns());
+#endif
                         break;
                     }
                     have_claim = true;
@@ -1610,6 +1728,8 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             }
         }
         SIMBA_CYC_END(p, ST_W_PLAN, cwp);
+        if (lane == 0 && od.phase_cands)
+            atomicAdd(p.planned, (unsigned long long)od.phase_cands);
         if (lane == 0 && !done)
             atomicAdd(&ps->active, 1u);
         __syncthreads();
@@ -1696,6 +1816,12 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
         __syncthreads();
     }
     flush_counts(p, ss.count, vis, ss.units, ss.rank_units);
+#ifdef SIMBA_CTA_TIMES
+    __syncthreads();
+    if (threadIdx.x == 0)
+        printf("CTA %d start %llu end %llu phases %u dry %llu\n", blockIdx.x, (unsigned long long)t0,
+               (unsigned long long)globaltimer_ns(), nphase, cta_dry);
+#endif
 }
 
 template <class W>
@@ -1706,7 +1832,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS) direct_kernel(const __grid
     const bool early = (p.mode == SIMBA_MODE_SEARCH) && !p.shuffled;
     const uint64_t t0 = globaltimer_ns();
     uint64_t my_count = 0, vis = 0;
-    uint64_t hint = p.nvirt / ((uint64_t)gridDim.x * (blockDim.x >> 5) * kGuide);
+    uint64_t hint = p.nvirt / ((uint64_t)gridDim.x * (blockDim.x >> 5) * p.guide);
     if (hint < 1)
         hint = 1;
     Claim cl;
@@ -1913,7 +2039,8 @@ void pool_put(int device, void *p, size_t bytes, bool host)
 struct simba_ctx {
     int device = 0, k = 0, w = 0, n = 0, max_size = 0;
     int wbytes = 4, R0 = 1, RG = 1, E = 1, kernel = 0;
-    int r0_up = MAXS + 1;  // first level whose units use R0 + 1
+    uint64_t r0_need = 0;  // a level's candidates per shard and launch from which it uses R0 + 1 (0: never)
+    int r0_up_env = 0;     // SIMBA_R0_UP override (diagnostics)
     uint32_t tbl_len = 0, gtbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
     unsigned char *d_gtbl = nullptr;
     int block_threads = 256, grid_unit = 0, grid_direct = 0;
@@ -1928,6 +2055,7 @@ struct simba_ctx {
     Tabs *d_tabs = nullptr;
     unsigned char *d_blob = nullptr;
     unsigned long long *d_ctr = nullptr;
+    unsigned long long *d_pool = nullptr;  // returned piece ranges (late splitting), kPoolSlots x {state, a, b}
     unsigned long long *h_ctr = nullptr;
     int32_t *d_tok = nullptr;
     unsigned long long *d_stats = nullptr;  // path statistics (SIMBA_STATS builds)
@@ -2096,7 +2224,28 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.n = c->n;
     p.s = rq.size;
     p.R0 = c->R0;  // min(R0 (+1 from level r0_up), s) per level in the kernel
-    p.r0_up = c->r0_up;
+    // per-launch shape: levels whose share of this launch (per shard) is large
+    // use R0 + 1; large launches use larger descriptors and claims
+    const uint64_t per_shard = range / rq.nshards;
+    p.r0_up = MAXS + 1;
+    if (c->r0_need) {
+        uint64_t vb = 0;  // virtual base of level s
+        for (int s = 1; s <= rq.size; ++s) {
+            const uint64_t T = row_total(c, s);
+            if (s >= s_lo) {
+                const uint64_t a = std::max(vb, rq.lo), b = std::min(vb + T, rq.hi);
+                if (b > a && (b - a) / rq.nshards >= c->r0_need) {
+                    p.r0_up = s;
+                    break;
+                }
+                vb += T;
+            }
+        }
+    }
+    if (c->r0_up_env)
+        p.r0_up = c->r0_up_env;
+    p.desc_cands = per_shard >= kBigLaunch ? kDescCandsBig : kDescCandsBig / 2;
+    p.guide = per_shard >= kBigLaunch ? kGuideBig : 2 * kGuideBig;
     p.s_lo = s_lo;
     p.s_hi = rq.size;
     p.vbase = c->d_lvl + kLvlWords;  // the level bases follow the per-level counters
@@ -2126,6 +2275,8 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.visited = c->d_ctr + 3;
     p.units = c->d_ctr + 4;
     p.flags = reinterpret_cast<unsigned int *>(c->d_ctr + 6);
+    p.planned = c->d_ctr + 7;
+    p.pool = c->d_pool;
     p.stats = c->d_stats;
     p.queue = c->d_queue;
     p.qcap = c->qcap;
@@ -2135,6 +2286,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     BlobInfo bi{c->d_blob, c->tbl_bytes, c->ex_bytes};
     const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(c->d_ctr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->d_pool, 0, sizeof(unsigned long long) * 3 * kPoolSlots, c->stream));
     c->h2d_bytes += sizeof(init);
     for (int z = 0; z <= MAXS; ++z) {  // per level: count, visited, first rank
         c->h_lvl[z] = 0;
@@ -2399,17 +2551,10 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     // levels with at least T[R0+1] * 2^18 candidates use R0 + 1 (rows of
     // T[R0+1] columns; fewer, larger units where the level is large enough
     // that its claims still span many rows)
-    c->r0_up = MAXS + 1;
-    if (o.r0 == 0 && R0 + 1 <= RG) {
-        const uint64_t need = t.T[R0 + 1] << 18;
-        for (int s = 1; s <= max_size; ++s)
-            if (t.T[s] >= need) {
-                c->r0_up = s;
-                break;
-            }
-    }
+    c->r0_need = (o.r0 == 0 && R0 + 1 <= RG) ? (t.T[R0 + 1] << SIMBA_R0_SHIFT) : 0;
+    c->r0_up_env = 0;
     if (const char *e = getenv("SIMBA_R0_UP"))
-        c->r0_up = atoi(e);
+        c->r0_up_env = atoi(e);
     {
         uint32_t off = 0, soff = 0;
         for (int z = 1; z <= MAXS; ++z) {
@@ -2479,7 +2624,8 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         const size_t o_queue = up(o_stats + sizeof(unsigned long long) * 2 * ST_N);
         const size_t o_vq = up(o_queue + db * c->qcap * (size_t)sms * 2);  // two CTAs per SM at most
         const size_t o_lvl = up(o_vq + sizeof(unsigned long long) * kVerifyCap * (size_t)sms * 2);
-        const size_t total = up(o_lvl + sizeof(unsigned long long) * (kLvlWords + MAXS + 2));
+        const size_t o_pool = up(o_lvl + sizeof(unsigned long long) * (kLvlWords + MAXS + 2));
+        const size_t total = up(o_pool + sizeof(unsigned long long) * 3 * kPoolSlots);
         unsigned char *base = (unsigned char *)pool_get(c->device, total, false, &c->arena_bytes, &e);
         if (!base)
             return cuda_bail(e, "cudaMalloc(context arena)");
@@ -2493,6 +2639,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         c->d_queue = base + o_queue;
         c->d_vq = reinterpret_cast<unsigned long long *>(base + o_vq);
         c->d_lvl = reinterpret_cast<unsigned long long *>(base + o_lvl);
+        c->d_pool = reinterpret_cast<unsigned long long *>(base + o_pool);
         if ((e = cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 2 * ST_N, c->stream)) != cudaSuccess)
             return cuda_bail(e, "cudaMemsetAsync(stats)");
         size_t hb = 0;

@@ -72,6 +72,8 @@ struct KParams {
     uint32_t gtbl_len;       // entries of sizes <= RG per example (global)
     int k, n, s, R0, RG, E;
     int r0_up;               // levels >= r0_up use R0 + 1
+    uint32_t guide;          // claim ~ remaining / (warps * guide)
+    uint64_t desc_cands;     // candidates per tile descriptor (at most)
     int mode;                // SIMBA_MODE_*
     int shuffled;
     uint64_t mask;
@@ -87,7 +89,9 @@ struct KParams {
     unsigned long long *count;    // satisfying candidates
     unsigned long long *visited;  // candidates evaluated
     unsigned long long *units;    // [0] units decoded, [1] units on the per-rank path
-    unsigned int *flags;          // bit 0: stopped by the time budget
+    unsigned int *flags;
+    unsigned long long *planned;  // candidates queued so far (all CTAs): phase budgets
+    unsigned long long *pool;     // returned piece ranges (late splitting)          // bit 0: stopped by the time budget
     unsigned long long *stats;    // [2*path] calls, [2*path+1] candidates (SIMBA_STATS builds)
     void *queue;                  // tile descriptors, qcap per CTA (plan/execute phases)
     uint32_t qcap;
@@ -560,6 +564,7 @@ struct Odometer {
     bool so0_bw;           // innermost outer segment has a bitwise part
     uint32_t gen;          // bumped whenever the outer chain (so) is recomposed
     bool ovf_o, ovf_l;
+    uint64_t phase_budget, phase_cands;  // candidates the warp may plan / has planned in this phase
     // planner resume point inside a 2-D row group (queue filled mid-group)
     bool rs_valid;
     uint32_t rs_c;

@@ -113,9 +113,9 @@ def test_identity_and_not_found_stats():
 
 
 def test_time_budget():
-    # a budget the device cannot meet: k=3 up to size 13 is ~1.2e11 candidates
+    # a budget the device cannot meet: k=3 up to size 14 is ~1.1e12 candidates
     spec = S.Specification.of([((i, i + 1, i + 2), (31 * i + 7) & 0xFFFFFFFF) for i in range(16)], k=3)
-    out = S.synthesize(spec, S.build(3, 13), S.EngineConfig(size_bound=13, time_budget=0.02))
+    out = S.synthesize(spec, S.build(3, 14), S.EngineConfig(size_bound=14, time_budget=0.01))
     assert out.status is S.Status.TIMED_OUT and out.expr is None
     # an expired budget never masks a hit in the current block (test_engine.py:122-130)
     ident = S.Specification.of([((v,), v) for v in (3, 9)], k=1)
