@@ -82,7 +82,7 @@ int fail(int code, const char *fmt, ...)
     } while (0)
 
 constexpr uint64_t kShuffleMult = 2246822507ULL;  // codec.py:29
-constexpr int kCtrWords = 8;  // ctr, best, count, visited, units[2], flags, planned
+constexpr int kCtrWords = 9;  // ctr, best, count, visited, units[0..1], flags, units[3] (example-0 hits), planned
 constexpr int kLvlWords = 3 * (SIMBA_MAX_SIZE + 1);  // per-level count, visited, first rank
 constexpr uint64_t kFuseCands = 1ull << 26;          // synthesize: levels fused per launch up to this many candidates
 constexpr uint64_t kSmemMax = 232448;  // opt-in dynamic shared memory per block (sm_100)
@@ -1728,7 +1728,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             }
         }
         SIMBA_CYC_END(p, ST_W_PLAN, cwp);
-        if (lane == 0 && od.phase_cands)
+        if (kPhaseGuide && lane == 0 && od.phase_cands)
             atomicAdd(p.planned, (unsigned long long)od.phase_cands);
         if (lane == 0 && !done)
             atomicAdd(&ps->active, 1u);
@@ -2275,7 +2275,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.visited = c->d_ctr + 3;
     p.units = c->d_ctr + 4;
     p.flags = reinterpret_cast<unsigned int *>(c->d_ctr + 6);
-    p.planned = c->d_ctr + 7;
+    p.planned = c->d_ctr + 8;
     p.pool = c->d_pool;
     p.stats = c->d_stats;
     p.queue = c->d_queue;
@@ -2284,7 +2284,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.vq = direct ? nullptr : c->d_vq;  // the per-rank kernel verifies inline
     p.vqcap = kVerifyCap;
     BlobInfo bi{c->d_blob, c->tbl_bytes, c->ex_bytes};
-    const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0};
+    const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(c->d_ctr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_pool, 0, sizeof(unsigned long long) * 3 * kPoolSlots, c->stream));
     c->h2d_bytes += sizeof(init);

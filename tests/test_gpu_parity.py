@@ -291,3 +291,25 @@ def test_enumerate_all_and_sampling():
         assert e.size == s
         r = encode(e, tab)
         assert S.decode(r.value, s, tab) == e
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,w,n,size", [(3, 6, 5, 7), (2, 4, 6, 8), (4, 32, 10, 6)])
+def test_example0_hits_counter_is_exact(k, w, n, size):
+    """The e-bar statistic's counter (candidates that match example 0, SURVEY.md
+    8(d)) equals the oracle's exhaustive count of the one-example spec."""
+    rng = random.Random(k * 100 + w)
+    pairs, seen = [], set()
+    while len(pairs) < n:
+        x = tuple(rng.getrandbits(w) for _ in range(k))
+        if x not in seen:
+            seen.add(x)
+            pairs.append((x, rng.getrandbits(w)))
+    spec = S.Specification(k=k, w=w, pairs=tuple(pairs))
+    tab = O.OracleTable(k, size)
+    with DeviceContext(spec, size) as ctx:
+        for s in range(1, size + 1):
+            r = ctx.count(s)
+            _, want, _, _ = O.scan_range(tab, k, w, pairs[:1], s, 0, tab.total(s), 0, tab.total(s),
+                                         threads=O.cpu_count())
+            assert r.ex0_hits == want, (s, r.ex0_hits, want)
