@@ -1463,31 +1463,54 @@ struct Claim {
 #endif
 constexpr uint64_t kSplitMin = SIMBA_SPLIT_MIN_LOG2 ? 1ull << SIMBA_SPLIT_MIN_LOG2 : 0;  // 0: no splitting
 
-__device__ __forceinline__ bool pool_push(const KParams &p, uint64_t a, uint64_t b, uint32_t start)
+// p.pool[0] counts full slots (a hint: pops skip an empty pool without a
+// scan); slot i occupies words 1 + 3i .. 3 + 3i.
+__device__ __forceinline__ unsigned long long *pool_slot(const KParams &p, uint32_t i)
+{
+    return p.pool + 1 + 3 * (i % kPoolSlots);
+}
+
+__device__ __forceinline__ bool pool_push(const KParams &p, uint64_t a, uint64_t b, uint32_t start)  // lane 0
 {
     for (uint32_t k = 0; k < kPoolSlots; ++k) {
-        unsigned long long *s = p.pool + 3 * ((start + k) % kPoolSlots);
-        if (atomicCAS(s, 0ull, 2ull) == 0ull) {
+        unsigned long long *s = pool_slot(p, start + k);
+        if (*(volatile unsigned long long *)s == 0ull && atomicCAS(s, 0ull, 2ull) == 0ull) {
             s[1] = a;
             s[2] = b;
             __threadfence();
             atomicExch(s, 1ull);
+            atomicAdd(p.pool, 1ull);
             return true;
         }
     }
     return false;
 }
 
-__device__ __forceinline__ bool pool_pop(const KParams &p, uint64_t &a, uint64_t &b, uint32_t start)
+// whole warp: the lanes scan 32 slots at a time
+__device__ __forceinline__ bool pool_pop(const KParams &p, uint64_t &a, uint64_t &b, uint32_t start, int lane)
 {
-    for (uint32_t k = 0; k < kPoolSlots; ++k) {
-        unsigned long long *s = p.pool + 3 * ((start + k) % kPoolSlots);
-        if (*(volatile unsigned long long *)s == 1ull && atomicCAS(s, 1ull, 3ull) == 1ull) {
-            __threadfence();
-            a = *(volatile unsigned long long *)(s + 1);
-            b = *(volatile unsigned long long *)(s + 2);
-            atomicExch(s, 0ull);
-            return true;
+    if (*(volatile unsigned long long *)p.pool == 0ull)
+        return false;
+    for (uint32_t k = 0; k < kPoolSlots; k += 32) {
+        unsigned long long *s = pool_slot(p, start + k + lane);
+        unsigned full = __ballot_sync(FULL, *(volatile unsigned long long *)s == 1ull);
+        while (full) {
+            const int src = __ffs(full) - 1;
+            full &= full - 1;
+            int won = 0;
+            if (lane == src && atomicCAS(s, 1ull, 3ull) == 1ull) {
+                __threadfence();
+                a = *(volatile unsigned long long *)(s + 1);
+                b = *(volatile unsigned long long *)(s + 2);
+                atomicExch(s, 0ull);
+                atomicAdd(p.pool, ~0ull);  // -1
+                won = 1;
+            }
+            if (__shfl_sync(FULL, won, src)) {
+                a = __shfl_sync(FULL, a, src);
+                b = __shfl_sync(FULL, b, src);
+                return true;
+            }
         }
     }
     return false;
@@ -1660,12 +1683,11 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                     // claims first, then ranges other warps returned to the pool
                     uint64_t pa = 0, pb = 0;
                     int got = claim_run(p, t0, hint, cl) ? 1 : 0;
-                    if (!got && lane == 0)
-                        got = pool_pop(p, pa, pb, gw * 7u) ? 2 : 0;
-                    got = __shfl_sync(FULL, got, 0);
+                    if (!got && kSplitMin)
+                        got = pool_pop(p, pa, pb, gw * 32u, lane) ? 2 : 0;
                     if (got == 2) {
-                        c0 = __shfl_sync(FULL, pa, 0);
-                        c1 = __shfl_sync(FULL, pb, 0);
+                        c0 = pa;
+                        c1 = pb;
                         have_claim = false;
                         if (early && c0 > read_best(p))
                             continue;  // ranks above a hit
@@ -2286,7 +2308,8 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     BlobInfo bi{c->d_blob, c->tbl_bytes, c->ex_bytes};
     const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(c->d_ctr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemsetAsync(c->d_pool, 0, sizeof(unsigned long long) * 3 * kPoolSlots, c->stream));
+    if (kSplitMin)
+        CK(cudaMemsetAsync(c->d_pool, 0, sizeof(unsigned long long) * (1 + 3 * kPoolSlots), c->stream));
     c->h2d_bytes += sizeof(init);
     for (int z = 0; z <= MAXS; ++z) {  // per level: count, visited, first rank
         c->h_lvl[z] = 0;
@@ -2625,7 +2648,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         const size_t o_vq = up(o_queue + db * c->qcap * (size_t)sms * 2);  // two CTAs per SM at most
         const size_t o_lvl = up(o_vq + sizeof(unsigned long long) * kVerifyCap * (size_t)sms * 2);
         const size_t o_pool = up(o_lvl + sizeof(unsigned long long) * (kLvlWords + MAXS + 2));
-        const size_t total = up(o_pool + sizeof(unsigned long long) * 3 * kPoolSlots);
+        const size_t total = up(o_pool + sizeof(unsigned long long) * (1 + 3 * kPoolSlots));
         unsigned char *base = (unsigned char *)pool_get(c->device, total, false, &c->arena_bytes, &e);
         if (!base)
             return cuda_bail(e, "cudaMalloc(context arena)");
