@@ -87,7 +87,7 @@ constexpr int kLvlWords = 3 * (SIMBA_MAX_SIZE + 1);  // per-level count, visited
 constexpr uint64_t kFuseCands = 1ull << 26;          // synthesize: levels fused per launch up to this many candidates
 constexpr uint64_t kSmemMax = 232448;  // opt-in dynamic shared memory per block (sm_100)
 #ifndef SIMBA_R0_SHIFT
-#define SIMBA_R0_SHIFT 16  // a level uses R0 + 1 from T[R0+1] * 2^SHIFT candidates per shard and launch
+#define SIMBA_R0_SHIFT 15  // a level uses R0 + 1 from T[R0+1] * 2^SHIFT candidates per shard and launch
 #endif
 constexpr uint32_t kPoolSlots = 1024;  // returned ranges (late splitting) per launch
 constexpr uint64_t kTblPad = 256;      // words after the global value table (8 x 32-lane reads past a row)
@@ -1526,7 +1526,10 @@ __device__ __forceinline__ bool pool_pop(const KParams &p, uint64_t &a, uint64_t
 // kBigLaunch candidates (fewer, longer claims: fewer rows cut at claim
 // boundaries), twice that below (shorter tails when the launch is short)
 constexpr uint32_t kGuideBig = SIMBA_GUIDE;
-constexpr uint64_t kBigLaunch = 40000000000ull;
+#ifndef SIMBA_BIG_LAUNCH
+#define SIMBA_BIG_LAUNCH 40000000000ull
+#endif
+constexpr uint64_t kBigLaunch = SIMBA_BIG_LAUNCH;
 
 __device__ __forceinline__ bool claim_run(const KParams &p, uint64_t t0, uint64_t &hint, Claim &cl)
 {
@@ -2249,8 +2252,13 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     // per-launch shape: levels whose share of this launch (per shard) is large
     // use R0 + 1; large launches use larger descriptors and claims
     const uint64_t per_shard = range / rq.nshards;
+    p.desc_cands = per_shard >= kBigLaunch ? kDescCandsBig : kDescCandsBig / 2;
+    p.guide = per_shard >= kBigLaunch ? kGuideBig : 2 * kGuideBig;
+    // R0 + 1 needs long claims: rows of T[R0+1] columns cut at every claim
+    // boundary, so the launch's first claims must span >= 16 such rows
+    const uint64_t claim0 = per_shard / (warps * p.guide);
     p.r0_up = MAXS + 1;
-    if (c->r0_need) {
+    if (c->r0_need && claim0 >= 16 * (c->r0_need >> SIMBA_R0_SHIFT)) {
         uint64_t vb = 0;  // virtual base of level s
         for (int s = 1; s <= rq.size; ++s) {
             const uint64_t T = row_total(c, s);
@@ -2266,8 +2274,6 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     }
     if (c->r0_up_env)
         p.r0_up = c->r0_up_env;
-    p.desc_cands = per_shard >= kBigLaunch ? kDescCandsBig : kDescCandsBig / 2;
-    p.guide = per_shard >= kBigLaunch ? kGuideBig : 2 * kGuideBig;
     p.s_lo = s_lo;
     p.s_hi = rq.size;
     p.vbase = c->d_lvl + kLvlWords;  // the level bases follow the per-level counters
