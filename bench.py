@@ -306,7 +306,7 @@ def main():
                     "issue_active_pct": prof.get("issue_active_pct"),
                     "note": "one masked-compare (LOP3.PAND) test per candidate and example evaluated: "
                             "the floor of this algorithm; ncu fields from the committed profile "
-                            "(profiles/ncu_unit_kernel.json, the size-13 level launched alone)"}}
+                            "(profiles/ncu_unit_kernel.json: this step's fused launch, C5 sizes 1..13)"}}
 
     # e2e through the public API: host spec -> context (H2D) -> scans -> D2H
     e2e = None
@@ -367,9 +367,9 @@ def C_double_pair(N, device):
 
 
 def profile_summary():
-    """Per-launch figures of the size-13 unit kernel from the committed ncu
-    summary (profiles/ncu_unit_kernel.json): DRAM bytes, warp instructions per
-    candidate, issue-active %."""
+    """Per-launch figures of the step's unit-kernel launch from the committed
+    ncu summary (profiles/ncu_unit_kernel.json, a copy of the fused-sweep
+    capture): DRAM bytes, warp instructions per candidate, issue-active %."""
     p = ROOT / "profiles" / "ncu_unit_kernel.json"
     out = {}
     try:
