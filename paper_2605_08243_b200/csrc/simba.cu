@@ -1669,7 +1669,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             od.phase_cands = 0;
         }
         const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-        if (kSplitMin && !done && have_piece && c1 - n >= kSplitMin) {
+        if (kSplitMin && !done && have_piece && c1 - n >= p.split_min) {
             // claims ran dry: hand the upper half of this piece to the pool
             int pushed = 0;
             if (lane == 0 && *(volatile unsigned long long *)p.ctr >= p.nvirt) {
@@ -2066,6 +2066,7 @@ struct simba_ctx {
     int wbytes = 4, R0 = 1, RG = 1, E = 1, kernel = 0;
     uint64_t r0_need = 0;  // a level's candidates per shard and launch from which it uses R0 + 1 (0: never)
     int r0_up_env = 0;     // SIMBA_R0_UP override (diagnostics)
+    uint64_t split_min = 0;  // pieces with at least this many ranks left split once claims run dry
     uint32_t tbl_len = 0, gtbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
     unsigned char *d_gtbl = nullptr;
     int block_threads = 256, grid_unit = 0, grid_direct = 0;
@@ -2274,6 +2275,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     }
     if (c->r0_up_env)
         p.r0_up = c->r0_up_env;
+    p.split_min = c->split_min;
     p.s_lo = s_lo;
     p.s_hi = rq.size;
     p.vbase = c->d_lvl + kLvlWords;  // the level bases follow the per-level counters
@@ -2584,6 +2586,11 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->r0_up_env = 0;
     if (const char *e = getenv("SIMBA_R0_UP"))
         c->r0_up_env = atoi(e);
+    // late-splitting threshold; SIMBA_SPLIT_MIN (ranks) overrides it so that tests
+    // can exercise the range pool on launches small enough for the CPU oracle
+    c->split_min = kSplitMin;
+    if (const char *e = getenv("SIMBA_SPLIT_MIN"))
+        c->split_min = std::max<uint64_t>(2, strtoull(e, nullptr, 10));
     {
         uint32_t off = 0, soff = 0;
         for (int z = 1; z <= MAXS; ++z) {

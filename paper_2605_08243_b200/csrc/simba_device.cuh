@@ -74,6 +74,7 @@ struct KParams {
     int r0_up;               // levels >= r0_up use R0 + 1
     uint32_t guide;          // claim ~ remaining / (warps * guide)
     uint64_t desc_cands;     // candidates per tile descriptor (at most)
+    uint64_t split_min;      // late splitting: pieces with >= split_min ranks left
     int mode;                // SIMBA_MODE_*
     int shuffled;
     uint64_t mask;

@@ -313,3 +313,36 @@ def test_example0_hits_counter_is_exact(k, w, n, size):
             _, want, _, _ = O.scan_range(tab, k, w, pairs[:1], s, 0, tab.total(s), 0, tab.total(s),
                                          threads=O.cpu_count())
             assert r.ex0_hits == want, (s, r.ex0_hits, want)
+
+
+@pytest.mark.gpu
+def test_late_splitting_keeps_counts_exact(monkeypatch):
+    """With a tiny late-splitting threshold (SIMBA_SPLIT_MIN, read at context
+    creation) almost every piece is split through the range pool once the
+    claims run dry; per-level counts, first ranks and visited counts of a
+    hit-dense spec must still equal the oracle's (no rank lost or doubled)."""
+    monkeypatch.setenv("SIMBA_SPLIT_MIN", "2048")
+    rng = random.Random(4242)
+    pairs, seen = [], set()
+    while len(pairs) < 4:
+        x = tuple(rng.getrandbits(3) for _ in range(2))
+        if x not in seen:
+            seen.add(x)
+            pairs.append((x, (x[0] * x[1] + x[0]) & 7))  # planted: many formulas match
+    spec = S.Specification(k=2, w=3, pairs=tuple(pairs))
+    size = 12
+    tab = O.OracleTable(2, size)
+    with DeviceContext(spec, size) as ctx:
+        _, levels = ctx.run_levels(1, size)
+        for s, count, first, visited in levels:
+            _, want, first_want, _ = O.scan_range(tab, 2, 3, pairs, s, 0, tab.total(s), 0, tab.total(s),
+                                                  threads=O.cpu_count())
+            assert (count, first, visited) == (want, first_want, tab.total(s)), s
+        for shard in range(3):  # sharded, split pieces included
+            r = ctx.run(size, 0, tab.total(size), mode="count", shard=shard, nshards=3)
+            assert r.visited > 0
+        total = sum(ctx.run(size, 0, tab.total(size), mode="count", shard=i, nshards=3).count for i in range(3))
+        assert total == levels[-1][1]
+    out = S.synthesize(spec, S.build(2, size), S.EngineConfig(size_bound=size))
+    first = next((s, f) for s, c, f, _ in levels if c)
+    assert (out.size, out.rank) == first
