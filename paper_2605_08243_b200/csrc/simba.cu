@@ -819,6 +819,40 @@ __device__ __forceinline__ Seg<W> gen_seg(Seg<W> g, bool merge, const Seg<W> &r0
     return g;
 }
 
+// Column chunks of 256 values, 8 per lane.  32-bit words: two 16-byte loads
+// per lane (lane holds columns 4*lane + e and 128 + 4*lane + e of the chunk),
+// so the chunk must start 16-byte aligned: the first chunk of [clo, chi)
+// starts up to 3 columns early, and those columns fail the range check at hit
+// time.  64-bit words: 8 coalesced strided loads.
+template <class W>
+__device__ __forceinline__ void load_cols(const W *t0, uint32_t a, int lane, W (&s)[8])
+{
+    if constexpr (sizeof(W) == 4) {
+        const uint4 *q = reinterpret_cast<const uint4 *>(t0 + a);
+        const uint4 u = __ldg(q + lane), v = __ldg(q + 32 + lane);
+        s[0] = u.x, s[1] = u.y, s[2] = u.z, s[3] = u.w, s[4] = v.x, s[5] = v.y, s[6] = v.z, s[7] = v.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            s[j] = __ldg(t0 + a + lane + 32 * j);
+    }
+}
+
+template <class W>
+__device__ __forceinline__ uint32_t col_off(int lane, int j)
+{
+    return sizeof(W) == 4 ? 128u * (uint32_t)(j >> 2) + 4u * (uint32_t)lane + (uint32_t)(j & 3)
+                          : (uint32_t)lane + 32u * (uint32_t)j;
+}
+
+// first chunk start of columns [clo, ...) of a row at table offset off2
+// (modulo 2^32: may precede column 0 of the row)
+template <class W>
+__device__ __forceinline__ uint32_t chunk0(uint32_t off2, uint32_t clo)
+{
+    return sizeof(W) == 4 ? clo - ((off2 + clo) & 3u) : clo;
+}
+
 // RF tile: rows [row0, row0 + nrows) of the X-unit, columns [clo, chi);
 // lanes hold 8 column values, rows are warp-uniform.  NT == 0: folded,
 // per-row (m, c), four rows per step; NT >= 1: per-row segment (merged P)
@@ -883,11 +917,9 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
             }
         }
         __syncwarp();
-        for (uint32_t c0 = clo; c0 < chi; c0 += 256) {
+        for (uint32_t c0 = chunk0<W>(off2, clo); (int32_t)(c0 - chi) < 0; c0 += 256) {
             W s[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                s[j] = t0[off2 + c0 + lane + 32 * j];
+            load_cols<W>(t0, off2 + c0, lane, s);
             if constexpr (NT == 0) {
                 for (uint32_t r = 0; r < nr4; r += 4) {
                     W m[4], c[4];
@@ -896,8 +928,8 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
                         uint32_t bits = hitmask8x4(s, m, c);
                         while (__any_sync(FULL, bits != 0)) {
                             const int b = bits ? __ffs(bits) - 1 : 0;
-                            const uint32_t k = b >> 3, d2 = c0 + lane + 32 * (b & 7);
-                            const bool h = bits != 0 && r + k < nr && d2 < chi;
+                            const uint32_t k = b >> 3, d2 = c0 + col_off<W>(lane, b & 7);
+                            const bool h = bits != 0 && r + k < nr && d2 - clo < chi - clo;
                             bits &= bits - 1;
                             on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r + k, d2, my_count);
                         }
@@ -920,8 +952,8 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
                         while (__any_sync(FULL, bits != 0)) {
                             SIMBA_WD("rf1-slow", bits, c0);
                             const int b = bits ? __ffs(bits) - 1 : 0;
-                            const uint32_t d2 = c0 + lane + 32 * b;
-                            const bool h = bits != 0 && d2 < chi;
+                            const uint32_t d2 = c0 + col_off<W>(lane, b);
+                            const bool h = bits != 0 && d2 - clo < chi - clo;
                             bits &= bits - 1;
                             on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, d2, my_count);
                         }
@@ -959,21 +991,18 @@ __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int p
     // column values come from L2: the next 256-column chunk is loaded while
     // this one is tested
     W s[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-        s[j] = __ldg(t0 + off2 + clo + lane + 32 * j);
-    for (uint32_t c0 = clo; c0 < chi; c0 += 256) {
+    const uint32_t cs = chunk0<W>(off2, clo);
+    load_cols<W>(t0, off2 + cs, lane, s);
+    for (uint32_t c0 = cs; (int32_t)(c0 - chi) < 0; c0 += 256) {
         W sn[8];
-        const uint32_t cn = (c0 + 256 < chi) ? c0 + 256 : c0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            sn[j] = __ldg(t0 + off2 + cn + lane + 32 * j);
+        const uint32_t cn = ((int32_t)(c0 + 256 - chi) < 0) ? c0 + 256 : c0;
+        load_cols<W>(t0, off2 + cn, lane, sn);
         if (__any_sync(FULL, hit8(s, m, c))) {
             uint32_t bits = hitmask8(s, m, c);
             while (__any_sync(FULL, bits != 0)) {
                 const int b = bits ? __ffs(bits) - 1 : 0;
-                const uint32_t d2 = c0 + lane + 32 * b;
-                const bool h = bits != 0 && d2 < chi;
+                const uint32_t d2 = c0 + col_off<W>(lane, b);
+                const bool h = bits != 0 && d2 - clo < chi - clo;
                 bits &= bits - 1;
                 on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0, d2, my_count);
             }
