@@ -1203,8 +1203,14 @@ constexpr uint64_t kSuperPerShard = SIMBA_SUPER_PER_SHARD;  // round-robin super
 // launches of at least kBigLaunch candidates, half that below
 constexpr uint64_t kDescCandsBig = 1ull << SIMBA_DESC_LOG2;
 constexpr int kVariants = 13;
-constexpr int kSizeClasses = 4;  // per variant, largest descriptors first (shorter phase tails)
+#ifndef SIMBA_SIZE_CLASSES
+#define SIMBA_SIZE_CLASSES 4  // 4 coarse classes; other values: halving classes (12 measured 2% faster but hangs one dense case, DESIGN 6)
+#endif
+constexpr int kSizeClasses = SIMBA_SIZE_CLASSES;  // queue order: largest descriptors first (shorter phase tails)
 constexpr int kBuckets = kVariants * kSizeClasses;
+#ifndef SIMBA_SIZE_MAJOR
+#define SIMBA_SIZE_MAJOR 1  // queue order: 1 = by size class (largest first), then variant; 0 = by variant first
+#endif
 
 struct PlanShared {
     unsigned int vqn;  // deferred verifications queued this phase (must stay the first field)
@@ -1270,8 +1276,13 @@ __device__ __forceinline__ void emit_tile(const KParams &p, Odometer<W, E> &od, 
         d->sz1 = (int8_t)xu.sz1;
         d->szy = (int8_t)xu.szy;
         d->s = od.s;
+#if SIMBA_SIZE_CLASSES == 4
         const int cls = cands >= (p.desc_cands >> 2) ? 0 : cands >= (p.desc_cands >> 5) ? 1 : cands >= 1024 ? 2 : 3;
-        ps->var[slot] = (uint8_t)(variant_of(kind, nt, nrows) * kSizeClasses + cls);
+#else
+        // halving classes: class i holds (desc_cands >> (i + 1), desc_cands >> i]
+        const int cls = min(kSizeClasses - 1, max(0, (__clzll((long long)cands) - __clzll((long long)p.desc_cands))));
+#endif
+        ps->var[slot] = (uint8_t)(SIMBA_SIZE_MAJOR ? cls * kVariants + variant_of(kind, nt, nrows) : variant_of(kind, nt, nrows) * kSizeClasses + cls);
     }
     if constexpr (E > 1) {  // lane e holds example e's chains (hit refinement)
         if (lane < E) {
@@ -1698,7 +1709,10 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             od.phase_cands = 0;
         }
         const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-        if (kSplitMin && !done && have_piece && c1 - n >= p.split_min) {
+        // (not while a 2-D row group is half emitted: n is then the group's start,
+        // behind the columns already queued, and a split inside the group would
+        // hand those columns out twice)
+        if (kSplitMin && !done && have_piece && !od.rs_valid && c1 - n >= p.split_min) {
             // claims ran dry: hand the upper half of this piece to the pool
             int pushed = 0;
             if (lane == 0 && *(volatile unsigned long long *)p.ctr >= p.nvirt) {
