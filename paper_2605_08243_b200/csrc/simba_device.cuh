@@ -490,7 +490,10 @@ struct SegStash {
 };
 
 // per-warp tile buffer: per-row (RF) or per-column (CF) test parameters
-constexpr int TILE_BUF = 128;
+#ifndef SIMBA_TILE_BUF
+#define SIMBA_TILE_BUF 128
+#endif
+constexpr int TILE_BUF = SIMBA_TILE_BUF;
 static_assert(TILE_BUF % 32 == 0, "rows are produced 32 per step");
 
 template <class W>
