@@ -86,6 +86,9 @@ constexpr int kCtrWords = 9;  // ctr, best, count, visited, units[0..1], flags, 
 constexpr int kLvlWords = 3 * (SIMBA_MAX_SIZE + 1);  // per-level count, visited, first rank
 constexpr uint64_t kFuseCands = 1ull << 26;          // synthesize: levels fused per launch up to this many candidates
 constexpr uint64_t kSmemMax = 232448;  // opt-in dynamic shared memory per block (sm_100)
+#ifndef SIMBA_R0_ROWS
+#define SIMBA_R0_ROWS 16  // R0 + 1 needs the launch's first claims to span this many rows of T[R0+1]
+#endif
 #ifndef SIMBA_R0_SHIFT
 #define SIMBA_R0_SHIFT 15  // a level uses R0 + 1 from T[R0+1] * 2^SHIFT candidates per shard and launch
 #endif
@@ -2302,7 +2305,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     // boundary, so the launch's first claims must span >= 16 such rows
     const uint64_t claim0 = per_shard / (warps * p.guide);
     p.r0_up = MAXS + 1;
-    if (c->r0_need && claim0 >= 16 * (c->r0_need >> SIMBA_R0_SHIFT)) {
+    if (c->r0_need && claim0 >= SIMBA_R0_ROWS * (c->r0_need >> SIMBA_R0_SHIFT)) {
         uint64_t vb = 0;  // virtual base of level s
         for (int s = 1; s <= rq.size; ++s) {
             const uint64_t T = row_total(c, s);
