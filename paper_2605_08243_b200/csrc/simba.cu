@@ -321,6 +321,14 @@ __device__ __noinline__ void on_hits(const KParams &p, const Staged &st, const S
     }
     if (hit) {
         const uint64_t rank = ubase + d1 * R2 + d2;
+#ifdef SIMBA_CHECKS
+        if (rank >= stabs()->T[s] || d2 >= R2) {
+            printf("SIMBA_CHECKS on_hits: s %d rank %llu T %llu ubase %llu d1 %llu R2 %u d2 %u pop %d block %d warp %d\n", s,
+                   (unsigned long long)rank, (unsigned long long)stabs()->T[s], (unsigned long long)ubase,
+                   (unsigned long long)d1, R2, d2, pop, blockIdx.x, threadIdx.x >> 5);
+            __trap();
+        }
+#endif
         if (!defer_check(p, p.vbase[s] + rank) && full_check<W>(p, st, rank, s))
             record_hit(p, s, rank, my_count);
     }
@@ -1330,8 +1338,14 @@ __device__ __noinline__ void exec_desc(const KParams &p, const Staged &st, const
         }
     }
     __syncwarp();
-#ifdef SIMBA_EMPTY_TILES
-    return;  // diagnostics: planning and queue traffic only
+#ifdef SIMBA_CHECKS
+    if (lane == 0 && (d->nrows == 0 || d->chi <= d->clo || d->chi > d->R2 || d->s < p.s_lo || d->s > p.s_hi ||
+                      d->ubase + (d->row0 + d->nrows) * (uint64_t)d->R2 > stabs()->T[d->s])) {
+        printf("SIMBA_CHECKS desc: kind %d s %d ubase %llu row0 %llu nrows %llu R2 %u clo %u chi %u nt %d pop %d\n",
+               d->kind, d->s, (unsigned long long)d->ubase, (unsigned long long)d->row0,
+               (unsigned long long)d->nrows, d->R2, d->clo, d->chi, d->nt, d->pop);
+        __trap();
+    }
 #endif
     const XU xu{d->x2d, d->pxop, d->szy, d->sz1, d->offy, d->off1, d->R1p};
     if (d->kind == 0)
