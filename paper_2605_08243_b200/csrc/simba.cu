@@ -1202,9 +1202,13 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 #endif
 constexpr int kDescPerWarp = SIMBA_DPW;
 #ifndef SIMBA_PHASE_GUIDE
-#define SIMBA_PHASE_GUIDE 0  // 0: no phase budget (measured best for single launches)
+#define SIMBA_PHASE_GUIDE 0  // unsharded launches: 0 = no phase budget (measured best for single launches)
 #endif
-constexpr uint64_t kPhaseGuide = SIMBA_PHASE_GUIDE;  // phase budget ~ remaining / (warps * kPhaseGuide)
+#ifndef SIMBA_SHARD_PHASE_GUIDE
+#define SIMBA_SHARD_PHASE_GUIDE 1  // sharded launches (nshards > 1): 8-way shards 4.47 -> 4.22 ms
+#endif
+constexpr uint64_t kPhaseGuide = SIMBA_PHASE_GUIDE;  // phase budget ~ remaining / (warps * guide)
+constexpr uint64_t kShardPhaseGuide = SIMBA_SHARD_PHASE_GUIDE;
 constexpr uint32_t kVerifyCap = 8192;  // deferred verifications per CTA and phase
 #ifndef SIMBA_SUPER_PER_SHARD
 #define SIMBA_SUPER_PER_SHARD 16
@@ -1697,6 +1701,8 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     uint64_t v = 0, c0 = 0, c1 = 0, n = 0;  // virtual ranks
 #ifdef SIMBA_CTA_TIMES
     unsigned int nphase = 0;
+    // longest plan and execute parts of a phase (thread 0): start, duration, queue size
+    unsigned long long tp0 = 0, tx0 = 0, mp_at = 0, mp_ns = 0, mx_at = 0, mx_ns = 0, mx_q = 0;
     __shared__ unsigned long long cta_dry;  // first time a warp of this CTA found no claim
     if (threadIdx.x == 0)
         cta_dry = ~0ull;
@@ -1705,6 +1711,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     for (;;) {
 #ifdef SIMBA_CTA_TIMES
         ++nphase;
+        tp0 = globaltimer_ns();
 #endif
         // ---- plan: advance the odometer, queue up to kDescPerWarp tiles
         SIMBA_WD("phase", n, c1);
@@ -1720,9 +1727,9 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             planned = __shfl_sync(FULL, planned, 0);
             const uint64_t all = p.nvirt * p.chunk_len;
             const uint64_t rem = all - min((uint64_t)planned, all);
-            od.phase_budget = kPhaseGuide == 0 ? ~0ull
-                                               : max(p.desc_cands, rem / ((uint64_t)gridDim.x * (blockDim.x >> 5) *
-                                                                          (kPhaseGuide ? kPhaseGuide : 1)));
+            od.phase_budget = p.phase_guide == 0
+                                  ? ~0ull
+                                  : max(p.desc_cands, rem / ((uint64_t)gridDim.x * (blockDim.x >> 5) * p.phase_guide));
             od.phase_cands = 0;
         }
         const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1813,7 +1820,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             }
         }
         SIMBA_CYC_END(p, ST_W_PLAN, cwp);
-        if (kPhaseGuide && lane == 0 && od.phase_cands)
+        if (p.phase_guide && lane == 0 && od.phase_cands)
             atomicAdd(p.planned, (unsigned long long)od.phase_cands);
         if (lane == 0 && !done)
             atomicAdd(&ps->active, 1u);
@@ -1828,6 +1835,13 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
         const unsigned int nq = ps->qn;
         if (nq == 0 && ps->active == 0)
             break;  // uniform: every warp is done and nothing is queued
+#ifdef SIMBA_CTA_TIMES
+        tx0 = globaltimer_ns();
+        if (tx0 - tp0 > mp_ns) {
+            mp_ns = tx0 - tp0;
+            mp_at = tp0;
+        }
+#endif
         // ---- sort the queue by tile variant (counting sort, warp 0)
         if (threadIdx.x < 32) {
             for (int k = lane; k < kBuckets; k += 32)
@@ -1864,6 +1878,16 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
         }
         SIMBA_CYC_END(p, ST_W_EXEC, cwe);
         __syncthreads();
+#ifdef SIMBA_CTA_TIMES
+        {
+            const unsigned long long tx1 = globaltimer_ns();
+            if (tx1 - tx0 > mx_ns) {
+                mx_ns = tx1 - tx0;
+                mx_at = tx0;
+                mx_q = nq;
+            }
+        }
+#endif
 #ifdef SIMBA_STATS
         if (threadIdx.x == 0) {
             atomicAdd(&p.stats[2 * ST_PH_EXEC], 1ull);
@@ -1904,8 +1928,9 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
 #ifdef SIMBA_CTA_TIMES
     __syncthreads();
     if (threadIdx.x == 0)
-        printf("CTA %d start %llu end %llu phases %u dry %llu\n", blockIdx.x, (unsigned long long)t0,
-               (unsigned long long)globaltimer_ns(), nphase, cta_dry);
+        printf("CTA %d start %llu end %llu phases %u dry %llu plan_max %llu at %llu exec_max %llu at %llu q %llu\n",
+               blockIdx.x, (unsigned long long)t0, (unsigned long long)globaltimer_ns(), nphase, cta_dry, mp_ns, mp_at,
+               mx_ns, mx_at, mx_q);
 #endif
 }
 
@@ -2336,6 +2361,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     if (c->r0_up_env)
         p.r0_up = c->r0_up_env;
     p.split_min = c->split_min;
+    p.phase_guide = rq.nshards > 1 ? kShardPhaseGuide : kPhaseGuide;
     p.s_lo = s_lo;
     p.s_hi = rq.size;
     p.vbase = c->d_lvl + kLvlWords;  // the level bases follow the per-level counters

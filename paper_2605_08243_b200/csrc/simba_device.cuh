@@ -75,6 +75,7 @@ struct KParams {
     uint32_t guide;          // claim ~ remaining / (warps * guide)
     uint64_t desc_cands;     // candidates per tile descriptor (at most)
     uint64_t split_min;      // late splitting: pieces with >= split_min ranks left
+    uint64_t phase_guide;    // phase budget ~ remaining / (warps * phase_guide); 0: none
     int mode;                // SIMBA_MODE_*
     int shuffled;
     uint64_t mask;
