@@ -1209,6 +1209,9 @@ constexpr int kDescPerWarp = SIMBA_DPW;
 #endif
 constexpr uint64_t kPhaseGuide = SIMBA_PHASE_GUIDE;  // phase budget ~ remaining / (warps * guide)
 constexpr uint64_t kShardPhaseGuide = SIMBA_SHARD_PHASE_GUIDE;
+#ifndef SIMBA_SHARD_GUIDE
+#define SIMBA_SHARD_GUIDE 4  // claim guide of sharded launches (0: the unsharded rule)
+#endif
 constexpr uint32_t kVerifyCap = 8192;  // deferred verifications per CTA and phase
 #ifndef SIMBA_SUPER_PER_SHARD
 #define SIMBA_SUPER_PER_SHARD 16
@@ -2151,6 +2154,7 @@ struct simba_ctx {
     int wbytes = 4, R0 = 1, RG = 1, E = 1, kernel = 0;
     uint64_t r0_need = 0;  // a level's candidates per shard and launch from which it uses R0 + 1 (0: never)
     int r0_up_env = 0;     // SIMBA_R0_UP override (diagnostics)
+    uint32_t guide_env = 0;  // SIMBA_GUIDE override of the claim guide (diagnostics)
     uint64_t split_min = 0;  // pieces with at least this many ranks left split once claims run dry
     uint32_t tbl_len = 0, gtbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
     unsigned char *d_gtbl = nullptr;
@@ -2340,6 +2344,10 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     const uint64_t per_shard = range / rq.nshards;
     p.desc_cands = per_shard >= kBigLaunch ? kDescCandsBig : kDescCandsBig / 2;
     p.guide = per_shard >= kBigLaunch ? kGuideBig : 2 * kGuideBig;
+#if SIMBA_SHARD_GUIDE
+    if (rq.nshards > 1)
+        p.guide = SIMBA_SHARD_GUIDE;
+#endif
     // R0 + 1 needs long claims: rows of T[R0+1] columns cut at every claim
     // boundary, so the launch's first claims must span >= 16 such rows
     const uint64_t claim0 = per_shard / (warps * p.guide);
@@ -2360,6 +2368,8 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     }
     if (c->r0_up_env)
         p.r0_up = c->r0_up_env;
+    if (c->guide_env)
+        p.guide = c->guide_env;
     p.split_min = c->split_min;
     p.phase_guide = rq.nshards > 1 ? kShardPhaseGuide : kPhaseGuide;
     p.s_lo = s_lo;
@@ -2672,6 +2682,9 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->r0_up_env = 0;
     if (const char *e = getenv("SIMBA_R0_UP"))
         c->r0_up_env = atoi(e);
+    c->guide_env = 0;
+    if (const char *e = getenv("SIMBA_GUIDE"))
+        c->guide_env = (uint32_t)std::max(1, atoi(e));
     // late-splitting threshold; SIMBA_SPLIT_MIN (ranks) overrides it so that tests
     // can exercise the range pool on launches small enough for the CPU oracle
     c->split_min = kSplitMin;
