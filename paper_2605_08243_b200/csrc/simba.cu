@@ -2155,6 +2155,7 @@ struct simba_ctx {
     uint64_t r0_need = 0;  // a level's candidates per shard and launch from which it uses R0 + 1 (0: never)
     int r0_up_env = 0;     // SIMBA_R0_UP override (diagnostics)
     uint32_t guide_env = 0;  // SIMBA_GUIDE override of the claim guide (diagnostics)
+    uint64_t last_super = 0;  // ranks per round-robin super-chunk of the last request
     uint64_t split_min = 0;  // pieces with at least this many ranks left split once claims run dry
     uint32_t tbl_len = 0, gtbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
     unsigned char *d_gtbl = nullptr;
@@ -2329,6 +2330,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     }
     const uint64_t nchunks = (range + chunk - 1) / chunk;
     const uint64_t nsuper = (nchunks + spc - 1) / spc;
+    c->last_super = spc * chunk;
     const uint64_t owned = (rq.shard < nsuper) ? (nsuper - rq.shard + rq.nshards - 1) / rq.nshards : 0;
     KParams p{};
     p.tabs = c->d_tabs;
@@ -2952,15 +2954,27 @@ int simba_run_levels(simba_ctx *c, int size_lo, int size_hi, int mode, uint64_t 
         return rc;
     // per-level visited: the request's visited candidates fill the levels in
     // order (claims ascend; COUNT mode visits every level completely, SEARCH
-    // mode every level below the found one)
-    uint64_t left = out->visited;
+    // mode every level below the found one); a shard owns the super-chunks
+    // g = shard, shard + nshards, ... of [0, tot), so its share of level z is
+    // its super-chunks' overlap with the level's virtual range
+    uint64_t left = out->visited, vb = 0;
+    const uint64_t sup = c->last_super, nsh = rq.nshards;
     for (int z = size_lo; z <= size_hi; ++z) {
         simba_level &lv = levels[z - size_lo];
+        const uint64_t T = row_total(c, z);
+        uint64_t own = T;
+        if (nsh > 1 && sup) {
+            own = 0;
+            for (uint64_t g = vb / sup; g * sup < vb + T; ++g)
+                if (g % nsh == shard)
+                    own += std::min(vb + T, (g + 1) * sup) - std::max(vb, g * sup);
+        }
         lv.size = z;
         lv.count = c->h_lvl[z];
-        lv.visited = std::min<uint64_t>(left, row_total(c, z));
+        lv.visited = std::min<uint64_t>(left, own);
         left -= lv.visited;
         lv.first_rank = c->h_lvl[2 * (MAXS + 1) + z];
+        vb += T;
     }
     return SIMBA_OK;
 }

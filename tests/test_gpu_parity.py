@@ -346,3 +346,73 @@ def test_late_splitting_keeps_counts_exact(monkeypatch):
     out = S.synthesize(spec, S.build(2, size), S.EngineConfig(size_bound=size))
     first = next((s, f) for s, c, f, _ in levels if c)
     assert (out.size, out.rank) == first
+
+
+def test_fused_shards_partition_levels_exactly():
+    """Sharded fused launches (simba_run_levels with nshards > 1: the
+    multi-GPU bench path, with the shard phase budget and claim guide) must
+    partition every level's rank space exactly: per-level counts and visited
+    counts summed over shards, and the minimum first rank over shards, equal
+    the oracle's; in search mode the (size, rank) minimum over shards is the
+    oracle's first hit."""
+    rng = random.Random(4242)
+    pairs, seen = [], set()
+    while len(pairs) < 4:
+        x = tuple(rng.getrandbits(3) for _ in range(2))
+        if x not in seen:
+            seen.add(x)
+            pairs.append((x, (x[0] * x[1] + x[0]) & 7))  # hit-dense: many formulas match
+    spec = S.Specification(k=2, w=3, pairs=tuple(pairs))
+    size = 11
+    tab = O.OracleTable(2, size)
+    want = {}
+    for s in range(1, size + 1):
+        _, c, f, _ = O.scan_range(tab, 2, 3, pairs, s, 0, tab.total(s), 0, tab.total(s), threads=O.cpu_count())
+        want[s] = (c, f, tab.total(s))
+    first_hit = min((s, f) for s, (c, f, _) in want.items() if c)
+    with DeviceContext(spec, size) as ctx:
+        for nsh in (2, 3, 8):
+            got = {s: [0, None, 0] for s in range(1, size + 1)}
+            for i in range(nsh):
+                _, levels = ctx.run_levels(1, size, shard=i, nshards=nsh)
+                for s, c, f, v in levels:
+                    g = got[s]
+                    g[0] += c
+                    g[2] += v
+                    if f is not None and (g[1] is None or f < g[1]):
+                        g[1] = f
+            assert {s: tuple(g) for s, g in got.items()} == want, nsh
+            hits = []
+            for i in range(nsh):
+                r, _ = ctx.run_levels(1, size, mode="search", shard=i, nshards=nsh)
+                if r.best_rank is not None:
+                    hits.append((r.size, r.best_rank))
+            assert min(hits) == first_hit, nsh
+
+
+def test_fused_shards_c5_shape_cover_every_rank():
+    """C5 shape (k=4, w=32, n=10, random outputs), sizes 1..12 (1.2e10 ranks):
+    8-way sharded fused launches visit every rank of every level exactly once
+    and their counts add up to the single launch's."""
+    rng = random.Random(8243)
+    pairs, seen = [], set()
+    while len(pairs) < 10:
+        x = tuple(rng.getrandbits(32) for _ in range(4))
+        if x not in seen:
+            seen.add(x)
+            pairs.append((x, rng.getrandbits(32)))
+    spec = S.Specification(k=4, w=32, pairs=tuple(pairs))
+    size = 12
+    table = S.build(4, size)
+    with DeviceContext(spec, size) as ctx:
+        _, whole = ctx.run_levels(1, size)
+        assert [v for *_, v in whole] == [table.total(s) for s in range(1, size + 1)]
+        count = {s: 0 for s in range(1, size + 1)}
+        visited = {s: 0 for s in range(1, size + 1)}
+        for i in range(8):
+            _, levels = ctx.run_levels(1, size, shard=i, nshards=8)
+            for s, c, _, v in levels:
+                count[s] += c
+                visited[s] += v
+        assert visited == {s: table.total(s) for s in range(1, size + 1)}
+        assert count == {s: c for s, c, _, _ in whole}
