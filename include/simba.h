@@ -136,7 +136,9 @@ int simba_run(simba_ctx *ctx, const simba_range *req, simba_result *out);
  * level with a hit, then its smallest rank, exactly the reference's order --
  * and stops claiming above it; COUNT mode visits everything.  levels[i]
  * (i = s - size_lo) receives the level's count, first satisfying rank and
- * visited candidates (in SEARCH mode exact up to the found level); `out`
+ * visited candidates (in SEARCH mode exact up to the found level; with
+ * nshards > 1, this shard's share of the level, so the SUM over shards is
+ * the level's total); `out`
  * carries the totals, the found (size, rank, tokens) and the launch time. */
 typedef struct {
     int32_t size;
