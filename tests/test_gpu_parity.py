@@ -416,3 +416,36 @@ def test_fused_shards_c5_shape_cover_every_rank():
                 visited[s] += v
         assert visited == {s: table.total(s) for s in range(1, size + 1)}
         assert count == {s: c for s, c, _, _ in whole}
+
+
+def test_fused_shards_search_c5_shape_matches_single_launch():
+    """Search mode over 8 fused shards (the multi-GPU Algorithm 1): for planted
+    k=4 w=32 n=10 targets of sizes 7..10, the lexicographic (size, rank)
+    minimum over shards equals the single launch's answer and the
+    synthesize() outcome, and the shard holding it decodes the same tokens."""
+    from paper_2605_08243_b200 import codec, expr
+
+    rng = random.Random(20261017)
+    size = 10
+    table = S.build(4, size)
+    for target in (7, 8, 9, 10):
+        e = codec.sample_uniform(target, table, rng)
+        pairs, seen = [], set()
+        while len(pairs) < 10:
+            x = tuple(rng.getrandbits(32) for _ in range(4))
+            if x not in seen:
+                seen.add(x)
+                pairs.append((x, expr.evaluate(e, x, 32)))
+        spec = S.Specification(k=4, w=32, pairs=tuple(pairs))
+        with DeviceContext(spec, size) as ctx:
+            one, _ = ctx.run_levels(1, size, mode="search")
+            assert one.best_rank is not None
+            best = None
+            for i in range(8):
+                r, _ = ctx.run_levels(1, size, mode="search", shard=i, nshards=8)
+                if r.best_rank is not None and (best is None or (r.size, r.best_rank) < best[:2]):
+                    best = (r.size, r.best_rank, r.tokens)
+            assert best == (one.size, one.best_rank, one.tokens), target
+        out = S.synthesize(spec, table, S.EngineConfig(size_bound=size))
+        assert (out.size, out.rank) == best[:2], target
+        assert out.size <= target
