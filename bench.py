@@ -145,6 +145,46 @@ def cpu_sample(size_bound, budget_s=10.0, seed_offset=0):
                       f"oracle/simba_oracle.c with {threads} threads, {dt:.1f}s"}
 
 
+_PY_REF = r"""
+import json, os, sys, time
+from mbasynth import counting
+from mbasynth.engine import EngineConfig, Specification, synthesize, run_stats
+pairs, budget = json.loads(sys.argv[1]), float(sys.argv[2])
+spec = Specification(k=4, w=32, pairs=tuple((tuple(i), o) for i, o in pairs))
+workers = len(os.sched_getaffinity(0))
+t0 = time.perf_counter()
+out = synthesize(spec, counting.build(4, 13), EngineConfig(size_bound=13, workers=workers, time_budget=budget))
+wall = time.perf_counter() - t0
+st = run_stats(out)
+print(json.dumps({"status": out.status.value, "workers": workers, "wall_s": wall,
+                  "visited": st["total_candidates"], "rate_stats": st["candidates_per_second"],
+                  "sizes": [[x.size, x.candidates] for x in out.stats]}))
+"""
+
+
+def python_reference_sample(budget_s=20.0):
+    """The UNMODIFIED reference (Python, installed in baseline/_ref) through its
+    public synthesize() on the C5 unsat spec with workers = all host threads
+    and a time budget: its own per-size stats give candidates/s (the rate
+    SURVEY.md 6 quotes), measured on this host in this run."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "mbasynth").is_dir():
+        return {"unavailable": "reference not installed in baseline/_ref (DESIGN.md: reference install)"}
+    env = dict(os.environ, PYTHONPATH=str(ref))
+    try:
+        p = subprocess.run([sys.executable, "-c", _PY_REF, json.dumps([[list(i), o] for i, o in unsat_pairs()]),
+                            str(budget_s)], cwd=str(ref), env=env, capture_output=True, text=True,
+                           timeout=budget_s * 4 + 120)
+        d = json.loads(p.stdout.strip().splitlines()[-1])
+    except (subprocess.TimeoutExpired, ValueError, IndexError) as exc:
+        return {"unavailable": f"reference run failed: {exc!r}"[:200]}
+    return {"value": d["visited"] / d["wall_s"], "unit": UNIT, "cores": d["workers"], "kind": "reference",
+            "rate_per_size_stats": d["rate_stats"],
+            "sample": f"mbasynth.synthesize (unmodified, baseline/_ref) on the C5 unsat spec, workers={d['workers']}, "
+                      f"time_budget={budget_s:g}s: {d['status']}, {d['visited']} candidates in {d['wall_s']:.1f}s "
+                      f"wall (sizes swept {d['sizes']})"}
+
+
 def run_reference(args):
     rank = env_int("RANK", 0)
     if rank != 0:
@@ -156,6 +196,8 @@ def run_reference(args):
     cb = dict(samples[0])
     cb["value"] = value
     cb["sample"] = f"{args.steps} steps of: " + samples[0]["sample"]
+    # the reference's own Python path on the same host, for context
+    cb["python_reference"] = python_reference_sample(args.py_ref_s)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -192,6 +234,7 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tts", action="store_true")
+    ap.add_argument("--py-ref-s", type=float, default=15.0, help="time budget of the Python reference sample")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -283,30 +326,43 @@ def main():
     assert visited == cands_per_step, (visited, cands_per_step)
     value = cands_per_step * args.steps / (dev_ms * 1e-3)
 
-    # roofline of the (only) launch of a step: all levels, INT32 issue peak
-    peak_ops, peak_ms = C_double_pair(N, local)
+    # roofline of the (only) launch of a step: all levels, INT32 pipe peaks
+    peaks = int_peaks(N, local)
     ebar = 1.0 + launch["ex0"] / max(1, cands_per_step // world)
     k_ms = statistics.mean(klaunch)
     algo_ops = sum(t * s for s, t in enumerate(totals, start=1)) / world * ebar  # sum over levels of T[s] * s
     achieved = algo_ops / (k_ms * 1e-3)
-    prof = profile_summary()
     cand_s = (cands_per_step / world) / (k_ms * 1e-3)
-    roofline = {"bound": "int32", "achieved": achieved / 1e9, "peak": peak_ops / 1e9, "unit": "Gop/s",
-                "frac": achieved / peak_ops, "traffic": prof.get("dram_bytes_per_launch"),
-                "note": f"the step's unit_kernel launch (levels 1..{C}): sum_s T[s]/N x s tokens x e-bar={ebar:.6f} "
-                        f"integer ops (SURVEY.md 8(d)) / {k_ms:.3f} ms (CUDA events); peak = simba_int32_peak "
-                        "LOP3+IMAD issue rate measured on this GPU (no integer figure in MEASURED_PEAKS.json). "
-                        "frac > 1 because shared subtrees are evaluated once per row/column, so the kernel spends "
-                        "~1 LOP3 per candidate instead of s*e-bar ops (DESIGN.md 2); see 'per_candidate' for the "
-                        "instruction-level view",
-                "per_candidate": {
-                    "test_ops_per_s": cand_s * ebar / 1e9,
-                    "frac_of_peak": cand_s * ebar / peak_ops,
-                    "warp_inst_per_candidate": prof.get("warp_inst_per_candidate"),
-                    "issue_active_pct": prof.get("issue_active_pct"),
-                    "note": "one masked-compare (LOP3.PAND) test per candidate and example evaluated: "
-                            "the floor of this algorithm; ncu fields from the committed profile "
-                            "(profiles/ncu_unit_kernel.json: this step's fused launch, C5 sizes 1..13)"}}
+    sha = lib_sha16()
+    prof = profile_summary(sha)
+    sms = info.get("grid_blocks", 148)  # one CTA per SM
+    clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    issue_peak = sms * 4 * clk  # warp instructions/s: 1 per SMSP and cycle
+    hw = {
+        "test_op_frac": cand_s * ebar / peaks["alu"],
+        "test_op_note": "the one masked compare (LOP3.PAND) per candidate and example evaluated -- the "
+                        "algorithm's floor -- against the LOP3-only ALU-pipe peak measured in this run",
+        "warp_inst_per_candidate": prof.get("warp_inst_per_candidate"),
+        "issue_frac": (prof["warp_inst_per_candidate"] * cand_s / issue_peak
+                       if prof.get("warp_inst_per_candidate") else None),
+        "issue_note": "issued warp instructions/s (this run's candidates/s x the ncu instructions per candidate of "
+                      "this build) / (SMs x 4 schedulers x the SM clock sampled in this run)",
+        "alu_pipe_pct": prof.get("alu_pipe_pct"),
+        "issue_active_pct": prof.get("issue_active_pct"),
+        "profile": prof.get("file"), "profile_build": prof.get("build"), "build": sha,
+        "profile_matches_build": prof.get("build") == sha,
+    }
+    roofline = {"bound": "int32", "achieved": achieved / 1e9, "peak": peaks["alu"] / 1e9, "unit": "Gop/s",
+                "frac": achieved / peaks["alu"], "traffic": prof.get("dram_bytes_per_launch"),
+                "peak_dual": peaks["dual"] / 1e9,
+                "note": f"SURVEY.md 8(d): the step's unit_kernel launch (levels 1..{C}), sum_s T[s]/N x s tokens "
+                        f"x e-bar={ebar:.6f} integer ops / {k_ms:.3f} ms (CUDA events) against P_int32 = the "
+                        "LOP3-only ALU-pipe rate measured in this run (simba_int32_pipe_peak; peak_dual = LOP3+IMAD, "
+                        "the issue limit; MEASURED_PEAKS.json has no integer figure).  frac > 1 by construction: "
+                        "subtrees shared by a row or column are evaluated once and the ancestors are folded into "
+                        "the test, so the kernel spends ~1 LOP3 per candidate, not s*e-bar ops (DESIGN.md 2).  "
+                        "Efficiency is in 'hw'.",
+                "hw": hw}
 
     # e2e through the public API: host spec -> context (H2D) -> scans -> D2H
     e2e = None
@@ -343,6 +399,7 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_sample(C, budget_s=args.cpu_budget)
+        cpu["python_reference"] = python_reference_sample(args.py_ref_s)
 
     if rank == 0:
         line = {
@@ -361,84 +418,142 @@ def main():
     return 0
 
 
-def C_double_pair(N, device):
+def int_peaks(N, device):
+    """Integer pipe peaks measured on this GPU (simba_int32_pipe_peak):
+    LOP3-only (ALU pipe = SURVEY.md 8(d)'s P_int32) and LOP3+IMAD (ALU + FMA
+    pipes, the issue limit); best of three launches each."""
     import ctypes as C
 
-    ops, ms = C.c_double(), C.c_double()
-    N.check_rc(N.lib.simba_int32_peak(device, 4096, C.byref(ops), C.byref(ms)))
-    return ops.value, ms.value
-
-
-def profile_summary():
-    """Per-launch figures of the step's unit-kernel launch from the committed
-    ncu summary (profiles/ncu_unit_kernel.json, a copy of the fused-sweep
-    capture): DRAM bytes, warp instructions per candidate, issue-active %."""
-    p = ROOT / "profiles" / "ncu_unit_kernel.json"
     out = {}
+    for name, mode in (("alu", 0), ("dual", 1)):
+        best = 0.0
+        for _ in range(3):
+            ops, ms = C.c_double(), C.c_double()
+            N.check_rc(N.lib.simba_int32_pipe_peak(device, 8192, mode, C.byref(ops), C.byref(ms)))
+            best = max(best, ops.value)
+        out[name] = best
+    return out
+
+
+def lib_sha16():
+    import hashlib
+
+    from paper_2605_08243_b200 import _native as N
+
+    return hashlib.sha256(Path(N.LIB_PATH).read_bytes()).hexdigest()[:16]
+
+
+def profile_summary(sha):
+    """Per-launch figures of the step's unit-kernel launch from the committed
+    ncu summary (profiles/ncu_unit_kernel.json: the bench-step launch of a
+    given libsimba build, its sha recorded as "build"): DRAM bytes, warp
+    instructions per candidate, ALU-pipe and issue-active %.  The bench line
+    says whether that build is the one running (profile_matches_build)."""
+    p = ROOT / "profiles" / "ncu_unit_kernel.json"
+    out = {"file": str(p.relative_to(ROOT))}
     try:
         d = json.loads(p.read_text())
     except (OSError, ValueError):
         return out
+    out["build"] = d.get("libsimba_sha16")
     out["dram_bytes_per_launch"] = d.get("dram_bytes_per_launch")
     m = d.get("metrics", {})
-    try:
-        out["warp_inst_per_candidate"] = float(m["smsp__inst_executed.sum"][0]) / d["candidates_per_launch"]
-    except (KeyError, ValueError, TypeError, ZeroDivisionError):
-        pass
-    try:
-        out["issue_active_pct"] = float(m["smsp__issue_active.avg.pct_of_peak_sustained_active"][0])
-    except (KeyError, ValueError, TypeError):
-        pass
-    return out
 
+    def f(name):
+        try:
+            return float(m[name][0])
+        except (KeyError, ValueError, TypeError, IndexError):
+            return None
 
-def time_to_solve(S, C):
-    """Time-to-solution (synthesize, sizes 1..C, early exit) for the C5
-    targets of sizes 11..13 whose specs are pinned in tests/golden/windows.json."""
-    wins = json.loads((ROOT / "tests" / "golden" / "windows.json").read_text())
-    out = []
-    # one untimed search first: module load / first-context costs are per process
-    S.synthesize(S.Specification(k=K, w=W_BITS, pairs=unsat_pairs()), S.build(K, 5), S.EngineConfig(size_bound=5))
-    for r in wins:
-        if r.get("meta", {}).get("config") != "C5" or "target_rank" not in r.get("meta", {}):
-            continue
-        sp = r["spec"]
-        spec = S.Specification(k=sp["k"], w=sp["w"], pairs=tuple((tuple(i), o) for i, o in sp["pairs"]))
-        t0 = time.perf_counter()
-        o = S.synthesize(spec, S.build(sp["k"], C), S.EngineConfig(size_bound=C))
-        ms = (time.perf_counter() - t0) * 1e3
-        out.append({"target_size": r["size"], "found_size": o.size, "rank": o.rank, "ms": round(ms, 2)})
+    try:
+        out["warp_inst_per_candidate"] = f("smsp__inst_executed.sum") / d["candidates_per_launch"]
+    except (KeyError, TypeError, ZeroDivisionError):
+        pass
+    out["issue_active_pct"] = f("smsp__issue_active.avg.pct_of_peak_sustained_active")
+    out["alu_pipe_pct"] = f("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active")
     return out
 
 
 def c5_targets(S):
-    wins = json.loads((ROOT / "tests" / "golden" / "windows.json").read_text())
-    for r in wins:
-        if r.get("meta", {}).get("config") != "C5" or "target_rank" not in r.get("meta", {}):
-            continue
-        sp = r["spec"]
-        yield r["size"], S.Specification(k=sp["k"], w=sp["w"], pairs=tuple((tuple(i), o) for i, o in sp["pairs"]))
+    """The time-to-solve suite (BASELINE configs[4]): ten targets per size
+    11, 12, 13 drawn by the reference's own suite generator whose MINIMAL
+    solution size is that size, each with the oracle's answer pinned in
+    tests/golden/c5.json (make_c5_golden.py)."""
+    g = json.loads((ROOT / "tests" / "golden" / "c5.json").read_text())
+    for size in sorted(g["tts"], key=int):
+        for rec in g["tts"][size]:
+            sp = rec["spec"]
+            spec = S.Specification(k=sp["k"], w=sp["w"], pairs=tuple((tuple(i), o) for i, o in sp["pairs"]))
+            yield int(size), spec, rec
+
+
+def tts_summary(out):
+    by = {}
+    for r in out:
+        by.setdefault(r["target_size"], []).append(r)
+    return {str(s): {"n": len(rs), "median_ms": round(statistics.median(r["ms"] for r in rs), 2),
+                     "max_ms": round(max(r["ms"] for r in rs), 2),
+                     "cpu_oracle_median_s": round(statistics.median(r["cpu_oracle_s"] for r in rs), 1)}
+            for s, rs in sorted(by.items())}
+
+
+def _tts_record(target, rec, size, first, ms, **extra):
+    want = rec["oracle"]
+    if (size, first) != (want["size"], want["rank"]):
+        raise AssertionError(f"time-to-solve {rec['id']}: device ({size}, {first}) != oracle "
+                             f"({want['size']}, {want['rank']})")
+    return {"id": rec["id"], "target_size": target, "found_size": size, "rank": first, "ms": round(ms, 2),
+            "cpu_oracle_s": rec["oracle_s"], **extra}
+
+
+def time_to_solve(S, C):
+    """Time-to-solution of synthesize (sizes 1..C, early exit; context
+    creation included) on the 30-target suite, every answer asserted equal to
+    the oracle's."""
+    out = []
+    # one untimed search first: module load / first-context costs are per process
+    S.synthesize(S.Specification(k=K, w=W_BITS, pairs=unsat_pairs()), S.build(K, 5), S.EngineConfig(size_bound=5))
+    table = S.build(K, C)
+    for target, spec, rec in c5_targets(S):
+        t0 = time.perf_counter()
+        o = S.synthesize(spec, table, S.EngineConfig(size_bound=C))
+        ms = (time.perf_counter() - t0) * 1e3
+        out.append(_tts_record(target, rec, o.size, o.rank, ms))
+    return {"targets": out, "by_size": tts_summary(out),
+            "verified": "every (size, rank) equals the oracle's (tests/golden/c5.json)",
+            "cpu_oracle": "cpu_oracle_s: the multithreaded C oracle's Alg. 1 on the GPU box host (recorded when the "
+                          "golden was made, make_c5_golden.py)"}
 
 
 def time_to_solve_ranks(S, C, rank, world, local, rdev, allmax, barrier):
     """time_to_solve on N ranks: each rank binds the spec to
-    its GPU and runs its shard of sizes 1..C as one fused search launch; one
-    MIN exchange gives the (size, rank) answer (parallel.search_fused).  The
-    time is the max over ranks, context creation included like synthesize's."""
+    its GPU and runs its shard of sizes 1..C as one fused search launch, all
+    shards publishing hits to one shared minimum on rank 0's GPU (early exit
+    across GPUs); one MIN exchange gives the (size, rank) answer
+    (parallel.search_fused).  The time is the max over ranks, context
+    creation included like synthesize's."""
     from paper_2605_08243_b200 import parallel as P
     from paper_2605_08243_b200.engine import DeviceContext
 
+    shared = P.shared_minimum(rank, world, device=local)
     with DeviceContext(S.Specification(k=K, w=W_BITS, pairs=unsat_pairs()), 5, device=local) as ctx:
-        P.search_fused(P.device_levels(ctx), 5, rank, world, device=rdev)  # untimed first search
+        ctx.set_shared_minimum(shared)
+        P.search_fused(P.device_levels(ctx), 5, rank, world, device=rdev, shared=shared)  # untimed first search
+        ctx.set_shared_minimum(None)
     out = []
-    for target, spec in c5_targets(S):
+    for target, spec, rec in c5_targets(S):
         barrier()
         t0 = time.perf_counter()
         with DeviceContext(spec, C, device=local) as ctx:
-            size, first, _ = P.search_fused(P.device_levels(ctx), C, rank, world, device=rdev)
+            ctx.set_shared_minimum(shared)
+            size, first, _ = P.search_fused(P.device_levels(ctx), C, rank, world, device=rdev, shared=shared)
+            ctx.set_shared_minimum(None)
         ms = allmax(time.perf_counter() - t0) * 1e3
-        out.append({"target_size": target, "found_size": size, "rank": first, "ms": round(ms, 2), "ranks": world})
-    return out
+        out.append(_tts_record(target, rec, size, first, ms, ranks=world))
+    barrier()  # rank 0's word outlives every rank's searches
+    shared.close()
+    return {"targets": out, "by_size": tts_summary(out),
+            "verified": "every (size, rank) equals the oracle's (tests/golden/c5.json)"}
 
 
 if __name__ == "__main__":

@@ -150,6 +150,37 @@ typedef struct {
 int simba_run_levels(simba_ctx *ctx, int size_lo, int size_hi, int mode, uint64_t shard, uint64_t nshards,
                      double time_budget_s, simba_level *levels, simba_result *out);
 
+/* ---------------------------------------------------------------------- */
+/* Cross-GPU early exit of a sharded search                */
+/* ---------------------------------------------------------------------- */
+
+/* The reference stops after the first wave with a hit (engine.py:248-250);
+ * across GPUs the equivalent is one 8-byte minimum that every shard's kernel
+ * publishes its hits to (atomicMin, system scope: NVLink peer atomics) and
+ * folds into its own bound at every claim and phase, so that no shard keeps
+ * claiming above another shard's hit.  Attached contexts use it in SEARCH
+ * requests with nshards > 1 (simba_run, simba_run_levels); every context
+ * sharing one word must run the same request space (same levels), and the
+ * word must be reset (simba_xbest_reset, by one process, followed by a
+ * barrier) before each sharded search.
+ *
+ * A simba_xbest is that word.  simba_xbest_create allocates it on `device`
+ * (set to SIMBA_NO_RANK) and writes its CUDA IPC handle
+ * (SIMBA_XBEST_HANDLE_BYTES bytes) for the other processes of the job;
+ * simba_xbest_open maps a handle created by ANOTHER process into this one on
+ * `device` (peer access over NVLink when the devices differ).  Contexts of one
+ * process may share one simba_xbest directly.  simba_ctx_set_xbest attaches
+ * it to a context (NULL detaches); the creator must outlive every search that
+ * uses it, and a context must not outlive the simba_xbest it is attached to. */
+#define SIMBA_XBEST_HANDLE_BYTES 64
+typedef struct simba_xbest simba_xbest;
+int simba_xbest_create(int device, unsigned char *handle, simba_xbest **out);
+int simba_xbest_open(int device, const unsigned char *handle, simba_xbest **out);
+int simba_xbest_reset(simba_xbest *x);
+int simba_xbest_read(simba_xbest *x, uint64_t *value);
+void simba_xbest_destroy(simba_xbest *x);
+int simba_ctx_set_xbest(simba_ctx *ctx, simba_xbest *x);
+
 /* engine.synthesize (engine.py:190-276), Algorithm 1 on the device: sizes
  * 1..size_bound ascending, each size level scanned in rank order (operator
  * blocks are contiguous rank ranges in slot order, engine.py:175-187) with
@@ -193,6 +224,13 @@ int simba_ctx_stream(simba_ctx *ctx, void **stream);
 /* INT32 issue-rate probe (roofline denominator): independent LOP3->IMAD
  * chains on every SM; reports integer ops/s and the kernel time. */
 int simba_int32_peak(int device, int iters, double *ops_per_s, double *kernel_ms);
+
+/* Pipe-saturating integer probes: 16 independent single-instruction chains
+ * per thread on every SM.  mode 0: LOP3 only (the ALU pipe; SURVEY.md 8(d)'s
+ * P_int32, nominally 148 SMs x 64 lanes x clock); mode 1: LOP3 and IMAD
+ * interleaved (ALU + FMA pipes, the issue limit).  Reports thread-level
+ * integer ops/s and the kernel time. */
+int simba_int32_pipe_peak(int device, int iters, int mode, double *ops_per_s, double *kernel_ms);
 
 /* Diagnostics: per-path (calls, candidates) counters of the unit kernel since
  * the context was created, in path order RF-fold, RF-gen, RF-row, CF-fold,

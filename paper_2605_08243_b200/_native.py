@@ -22,6 +22,7 @@ TABLE_MAX = 64
 MODE_SEARCH, MODE_COUNT = 0, 1
 STATUS_FOUND, STATUS_NOT_FOUND, STATUS_TIMED_OUT = 0, 1, 2
 NO_RANK = (1 << 64) - 1
+XBEST_HANDLE_BYTES = 64
 
 
 class Options(C.Structure):
@@ -125,11 +126,18 @@ SIGNATURES = {
     "simba_ctx_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "simba_ctx_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int]),
     "simba_int32_peak": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "simba_int32_pipe_peak": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "simba_vfb_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                    C.c_uint64, C.c_int, C.POINTER(C.c_void_p)]),
     "simba_vfb_level": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.POINTER(VfbRow)]),
     "simba_vfb_tokens": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32), C.c_int, C.POINTER(C.c_int)]),
     "simba_vfb_destroy": (None, [C.c_void_p]),
+    "simba_xbest_create": (C.c_int, [C.c_int, C.POINTER(C.c_ubyte), C.POINTER(C.c_void_p)]),
+    "simba_xbest_open": (C.c_int, [C.c_int, C.POINTER(C.c_ubyte), C.POINTER(C.c_void_p)]),
+    "simba_xbest_reset": (C.c_int, [C.c_void_p]),
+    "simba_xbest_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "simba_xbest_destroy": (None, [C.c_void_p]),
+    "simba_ctx_set_xbest": (C.c_int, [C.c_void_p, C.c_void_p]),
     "simba_last_error": (C.c_char_p, []),
     "simba_device_count": (C.c_int, []),
     "simba_launch_count": (C.c_uint64, []),

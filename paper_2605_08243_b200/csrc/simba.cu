@@ -82,7 +82,8 @@ int fail(int code, const char *fmt, ...)
     } while (0)
 
 constexpr uint64_t kShuffleMult = 2246822507ULL;  // codec.py:29
-constexpr int kCtrWords = 9;  // ctr, best, count, visited, units[0..1], flags, units[3] (example-0 hits), planned
+constexpr int kCtrWords = 10;  // ctr, best, count, visited, units[0..1], flags, units[3] (example-0 hits), planned,
+                               // dropped (lowest rank of a run dropped by the time budget)
 constexpr int kLvlWords = 3 * (SIMBA_MAX_SIZE + 1);  // per-level count, visited, first rank
 constexpr uint64_t kFuseCands = 1ull << 26;          // synthesize: levels fused per launch up to this many candidates
 constexpr uint64_t kSmemMax = 232448;  // opt-in dynamic shared memory per block (sm_100)
@@ -164,6 +165,8 @@ __device__ __forceinline__ void record_hit(const KParams &p, int s, uint64_t ran
 {
     ++my_count;
     atomicMin(p.best, (unsigned long long)(p.vbase[s] + rank));
+    if (p.xbest)  // publish to the other shards (system scope: the word may live on a peer GPU)
+        atomicMin_system(p.xbest, (unsigned long long)(p.vbase[s] + rank));
     atomicAdd(&p.lvl[s], 1ull);
     atomicMin(&p.lvl[2 * (MAXS + 1) + s], (unsigned long long)rank);
 }
@@ -387,6 +390,20 @@ __device__ __forceinline__ W modinv_odd(W a)
     for (int i = 0; i < (sizeof(W) == 4 ? 4 : 5); ++i)
         x = x * ((W)2 - a * x);
     return x;
+}
+
+// Cross-shard early exit: fold the shared minimum of a sharded search into
+// this launch's best, so that claims, pieces and P blocks above another
+// shard's hit are skipped exactly as above a local one (one thread; called
+// per claim and per CTA phase, a handful of NVLink loads per millisecond).
+__device__ __forceinline__ void pull_xbest(const KParams &p)
+{
+    if (p.xbest) {
+        unsigned long long g;
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(g) : "l"(p.xbest) : "memory");
+        if (g < *(volatile unsigned long long *)p.best)
+            atomicMin(p.best, g);
+    }
 }
 
 __device__ __forceinline__ uint64_t read_best(const KParams &p)
@@ -1595,12 +1612,27 @@ constexpr uint32_t kGuideBig = SIMBA_GUIDE;
 #endif
 constexpr uint64_t kBigLaunch = SIMBA_BIG_LAUNCH;
 
+// real rank range of the contiguous piece of a run starting at virtual chunk v
+__device__ __forceinline__ void run_piece(const KParams &p, uint64_t v, uint64_t v1, uint64_t &c0, uint64_t &c1,
+                                          uint64_t &vnext)
+{
+    const uint64_t sc = v / p.spc, within = v - sc * p.spc;
+    const uint64_t pend = min(v1, (sc + 1) * p.spc);
+    const uint64_t rc = (p.shard + sc * p.nshards) * p.spc + within;
+    c0 = p.lo + rc * p.chunk_len;
+    c1 = min(p.lo + (rc + (pend - v)) * p.chunk_len, p.hi);
+    if (c0 > p.hi)
+        c0 = p.hi;
+    vnext = pend;
+}
+
 __device__ __forceinline__ bool claim_run(const KParams &p, uint64_t t0, uint64_t &hint, Claim &cl)
 {
     const int lane = threadIdx.x & 31;
     unsigned long long c = 0;
     int go = 1;
     if (lane == 0) {
+        pull_xbest(p);
         const uint64_t want = hint;
         c = atomicAdd(p.ctr, (unsigned long long)want);
         if (c >= p.nvirt) {
@@ -1616,6 +1648,12 @@ __device__ __forceinline__ bool claim_run(const KParams &p, uint64_t t0, uint64_
             // recorded hit; the very first run always proceeds (engine.py:251-258)
             if (p.budget_ns && c > 0 && *(volatile unsigned long long *)p.best == SIMBA_NO_RANK &&
                 globaltimer_ns() - t0 > p.budget_ns) {
+                // the lowest dropped rank decides whether a later hit is exact:
+                // CTAs read their clocks at slightly different times, so a run
+                // above this one may still record a hit (host: run_req)
+                uint64_t d0, d1, dn;
+                run_piece(p, cl.v0, cl.v1, d0, d1, dn);
+                atomicMin(p.dropped, (unsigned long long)d0);
                 atomicOr(p.flags, 1u);
                 go = 0;
             }
@@ -1626,20 +1664,6 @@ __device__ __forceinline__ bool claim_run(const KParams &p, uint64_t t0, uint64_
     cl.v1 = __shfl_sync(FULL, cl.v1, 0);
     hint = __shfl_sync(FULL, hint, 0);
     return go != 0;
-}
-
-// real rank range of the contiguous piece of a run starting at virtual chunk v
-__device__ __forceinline__ void run_piece(const KParams &p, uint64_t v, uint64_t v1, uint64_t &c0, uint64_t &c1,
-                                          uint64_t &vnext)
-{
-    const uint64_t sc = v / p.spc, within = v - sc * p.spc;
-    const uint64_t pend = min(v1, (sc + 1) * p.spc);
-    const uint64_t rc = (p.shard + sc * p.nshards) * p.spc + within;
-    c0 = p.lo + rc * p.chunk_len;
-    c1 = min(p.lo + (rc + (pend - v)) * p.chunk_len, p.hi);
-    if (c0 > p.hi)
-        c0 = p.hi;
-    vnext = pend;
 }
 
 __device__ __forceinline__ void flush_counts(const KParams &p, uint64_t my_count, uint64_t vis, uint64_t units,
@@ -1718,6 +1742,8 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
 #endif
         // ---- plan: advance the odometer, queue up to kDescPerWarp tiles
         SIMBA_WD("phase", n, c1);
+        if (threadIdx.x == 0)
+            pull_xbest(p);  // the other shards' hits (read_best below sees them)
         SIMBA_CYC_BEGIN(cph);
         SIMBA_CYC_BEGIN(cwp);
         int emitted = 0;
@@ -2015,6 +2041,40 @@ __global__ void __launch_bounds__(256) int32_peak_kernel(uint32_t seed, int iter
         out[0] = r;
 }
 
+// Pipe-saturating integer probes (the roofline denominators of DESIGN.md 5):
+// 16 independent chains per thread, one instruction per chain and step
+// (inline PTX, so nothing is fused or hoisted): MODE 0 = LOP3 only (the ALU
+// pipe: IADD3/LOP3/SHF, rt 2 cycles per SMSP), MODE 1 = LOP3 and IMAD chains
+// interleaved (ALU + FMA pipes: the issue limit of 1 warp instruction per
+// SMSP and cycle).  ops/s = threads * iters * 16 / time.
+template <int MODE>
+__global__ void __launch_bounds__(256) int_pipe_kernel(uint32_t seed, int iters, uint32_t *out)
+{
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t a[16], b[16], c[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        a[u] = seed * (tid + 1) + u;
+        b[u] = seed ^ (tid * 2654435761u + 7u * u);
+        c[u] = (seed + u) * 40503u;
+    }
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            if (MODE == 1 && (u & 1))
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[u]) : "r"(b[u]), "r"(c[u]));
+            else
+                asm volatile("lop3.b32 %0, %0, %1, %2, 0x6a;" : "+r"(a[u]) : "r"(b[u]), "r"(c[u]));
+        }
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+        r ^= a[u];
+    if (r == 0x12345678u)
+        out[0] = r;
+}
+
 __global__ void decode_kernel(const Tabs *tabs, uint64_t rank, int size, int32_t *out)
 {
     int8_t buf[MAXS];
@@ -2155,6 +2215,7 @@ struct simba_ctx {
     uint64_t r0_need = 0;  // a level's candidates per shard and launch from which it uses R0 + 1 (0: never)
     int r0_up_env = 0;     // SIMBA_R0_UP override (diagnostics)
     uint32_t guide_env = 0;  // SIMBA_GUIDE override of the claim guide (diagnostics)
+    uint64_t big_launch = 0;  // candidates per shard from which launches use the big shapes (SIMBA_BIG_LAUNCH)
     uint64_t last_super = 0;  // ranks per round-robin super-chunk of the last request
     uint64_t split_min = 0;  // pieces with at least this many ranks left split once claims run dry
     uint32_t tbl_len = 0, gtbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
@@ -2183,6 +2244,13 @@ struct simba_ctx {
     size_t arena_bytes = 0;
     uint32_t qcap = 0, ps_off = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this context
+    unsigned long long *xbest = nullptr;  // attached shared minimum of a sharded search (simba_xbest)
+};
+
+struct simba_xbest {
+    int device = 0;
+    unsigned long long *word = nullptr;
+    bool imported = false;  // an IPC mapping (close) or this process's allocation (free)
 };
 
 namespace {
@@ -2251,6 +2319,7 @@ struct Req {
     bool shuffled;
     uint64_t offset, block_total;
     bool direct;
+    bool xbest;  // sharded search: use the attached shared minimum
 };
 
 int decode_rank(simba_ctx *c, uint64_t rank, int size, int32_t *tokens)
@@ -2344,8 +2413,8 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     // per-launch shape: levels whose share of this launch (per shard) is large
     // use R0 + 1; large launches use larger descriptors and claims
     const uint64_t per_shard = range / rq.nshards;
-    p.desc_cands = per_shard >= kBigLaunch ? kDescCandsBig : kDescCandsBig / 2;
-    p.guide = per_shard >= kBigLaunch ? kGuideBig : 2 * kGuideBig;
+    p.desc_cands = per_shard >= c->big_launch ? kDescCandsBig : kDescCandsBig / 2;
+    p.guide = per_shard >= c->big_launch ? kGuideBig : 2 * kGuideBig;
 #if SIMBA_SHARD_GUIDE
     if (rq.nshards > 1)
         p.guide = SIMBA_SHARD_GUIDE;
@@ -2368,7 +2437,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
             }
         }
     }
-    if (c->r0_up_env)
+    if (c->r0_up_env && c->R0 + 1 <= c->RG)  // R0 + 1 column values come from the global table
         p.r0_up = c->r0_up_env;
     if (c->guide_env)
         p.guide = c->guide_env;
@@ -2404,6 +2473,8 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.units = c->d_ctr + 4;
     p.flags = reinterpret_cast<unsigned int *>(c->d_ctr + 6);
     p.planned = c->d_ctr + 8;
+    p.dropped = c->d_ctr + 9;
+    p.xbest = (rq.xbest && rq.mode == SIMBA_MODE_SEARCH && !rq.shuffled && rq.nshards > 1) ? c->xbest : nullptr;
     p.pool = c->d_pool;
     p.stats = c->d_stats;
     p.queue = c->d_queue;
@@ -2412,7 +2483,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.vq = direct ? nullptr : c->d_vq;  // the per-rank kernel verifies inline
     p.vqcap = kVerifyCap;
     BlobInfo bi{c->d_blob, c->tbl_bytes, c->ex_bytes};
-    const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0, 0};
+    const unsigned long long init[kCtrWords] = {0, SIMBA_NO_RANK, 0, 0, 0, 0, 0, 0, 0, SIMBA_NO_RANK};
     CK(cudaMemcpyAsync(c->d_ctr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
     if (kSplitMin)
         CK(cudaMemsetAsync(c->d_pool, 0, sizeof(unsigned long long) * (1 + 3 * kPoolSlots), c->stream));
@@ -2452,6 +2523,12 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     out->count = c->h_ctr[2];
     out->best_rank = c->h_ctr[1];
     out->completed = (c->h_ctr[6] & 1u) ? 0 : 1;
+    // A hit is the request's answer only if nothing below it was dropped by
+    // the time budget.  Otherwise the reference, scanning chunks in order,
+    // would have timed out before reaching it (engine.py:251-258); in shuffled
+    // order any dropped run leaves the block minimum unknown.
+    if (!out->completed && out->best_rank != SIMBA_NO_RANK && (rq.shuffled || c->h_ctr[9] < out->best_rank))
+        out->best_rank = SIMBA_NO_RANK;
     out->found = out->best_rank != SIMBA_NO_RANK;
     if (out->found) {  // virtual -> (level, in-size rank)
         int z = s_lo;
@@ -2684,6 +2761,12 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->r0_up_env = 0;
     if (const char *e = getenv("SIMBA_R0_UP"))
         c->r0_up_env = atoi(e);
+    // big-launch shapes (2^18-candidate descriptors, claim guide kGuideBig);
+    // SIMBA_BIG_LAUNCH (candidates per shard) lets tests force them on launches
+    // small enough for the CPU oracle
+    c->big_launch = kBigLaunch;
+    if (const char *e = getenv("SIMBA_BIG_LAUNCH"))
+        c->big_launch = strtoull(e, nullptr, 10);
     c->guide_env = 0;
     if (const char *e = getenv("SIMBA_GUIDE"))
         c->guide_env = (uint32_t)std::max(1, atoi(e));
@@ -2849,6 +2932,105 @@ void simba_ctx_destroy(simba_ctx *c)
     delete c;
 }
 
+int simba_xbest_create(int device, unsigned char *handle, simba_xbest **out)
+{
+    if (!handle || !out)
+        return fail(SIMBA_EINVAL, "null argument");
+    *out = nullptr;
+    CK(cudaSetDevice(device));
+    void *p = nullptr;
+    CK(cudaMalloc(&p, 256));  // its own allocation: an IPC handle names a whole allocation
+    const unsigned long long none = SIMBA_NO_RANK;
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaMemcpy(p, &none, sizeof(none), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return fail(SIMBA_ECUDA, "shared minimum: %s", cudaGetErrorString(e));
+    }
+    static_assert(sizeof(h) == SIMBA_XBEST_HANDLE_BYTES, "IPC handle size");
+    memcpy(handle, &h, sizeof(h));
+    simba_xbest *x = new simba_xbest;
+    x->device = device;
+    x->word = reinterpret_cast<unsigned long long *>(p);
+    *out = x;
+    return SIMBA_OK;
+}
+
+int simba_xbest_open(int device, const unsigned char *handle, simba_xbest **out)
+{
+    if (!handle || !out)
+        return fail(SIMBA_EINVAL, "null argument");
+    *out = nullptr;
+    CK(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void *p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+        return fail(SIMBA_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    simba_xbest *x = new simba_xbest;
+    x->device = device;
+    x->word = reinterpret_cast<unsigned long long *>(p);
+    x->imported = true;
+    *out = x;
+    return SIMBA_OK;
+}
+
+int simba_xbest_reset(simba_xbest *x)
+{
+    if (!x)
+        return fail(SIMBA_EINVAL, "null shared minimum");
+    CK(cudaSetDevice(x->device));
+    const unsigned long long none = SIMBA_NO_RANK;
+    CK(cudaMemcpy(x->word, &none, sizeof(none), cudaMemcpyHostToDevice));
+    return SIMBA_OK;
+}
+
+int simba_xbest_read(simba_xbest *x, uint64_t *value)
+{
+    if (!x || !value)
+        return fail(SIMBA_EINVAL, "null argument");
+    CK(cudaSetDevice(x->device));
+    unsigned long long v = 0;
+    CK(cudaMemcpy(&v, x->word, sizeof(v), cudaMemcpyDeviceToHost));
+    *value = v;
+    return SIMBA_OK;
+}
+
+void simba_xbest_destroy(simba_xbest *x)
+{
+    if (!x)
+        return;
+    cudaSetDevice(x->device);
+    if (x->imported)
+        cudaIpcCloseMemHandle(x->word);
+    else
+        cudaFree(x->word);
+    delete x;
+}
+
+int simba_ctx_set_xbest(simba_ctx *c, simba_xbest *x)
+{
+    if (!c)
+        return fail(SIMBA_EINVAL, "null context");
+    if (x && x->device != c->device) {
+        // another GPU's word in this process: NVLink peer access
+        int ok = 0;
+        CK(cudaDeviceCanAccessPeer(&ok, c->device, x->device));
+        if (!ok)
+            return fail(SIMBA_ECUDA, "device %d cannot access device %d", c->device, x->device);
+        CK(cudaSetDevice(c->device));
+        cudaError_t e = cudaDeviceEnablePeerAccess(x->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            return fail(SIMBA_ECUDA, "cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
+        cudaGetLastError();
+    }
+    c->xbest = x ? x->word : nullptr;
+    return SIMBA_OK;
+}
+
 int simba_ctx_info(simba_ctx *c, int *r0, int *rg, int *table_examples, int *word_bytes, int *grid_blocks,
                    int *block_threads, int *smem_bytes)
 {
@@ -2919,6 +3101,7 @@ int simba_run(simba_ctx *c, const simba_range *req, simba_result *out)
     rq.nshards = req->nshards ? req->nshards : 1;
     rq.stop_above = req->stop_above;
     rq.budget_s = req->time_budget_s;
+    rq.xbest = true;
     return run_req(c, rq, out);
 }
 
@@ -2949,6 +3132,7 @@ int simba_run_levels(simba_ctx *c, int size_lo, int size_hi, int mode, uint64_t 
     rq.nshards = nshards ? nshards : 1;
     rq.stop_above = SIMBA_NO_RANK;
     rq.budget_s = time_budget_s;
+    rq.xbest = true;
     const int rc = run_req(c, rq, out);
     if (rc)
         return rc;
@@ -3006,7 +3190,7 @@ int simba_synthesize(simba_ctx *c, int size_bound, int shuffled, double time_bud
         while (s_lo <= size_bound) {
             int s_hi = s_lo;
             uint64_t acc = row_total(c, s_lo);
-            while (s_hi < size_bound && acc + row_total(c, s_hi + 1) <= kFuseCands)
+            while (s_hi < size_bound && acc <= kFuseCands && row_total(c, s_hi + 1) <= kFuseCands - acc)
                 acc += row_total(c, ++s_hi);
             const auto t0 = clk::now();
             std::vector<simba_level> lv(s_hi - s_lo + 1);
@@ -3147,6 +3331,44 @@ int simba_ctx_stream(simba_ctx *c, void **stream)
     if (!c || !stream)
         return fail(SIMBA_EINVAL, "null argument");
     *stream = (void *)c->stream;
+    return SIMBA_OK;
+}
+
+int simba_int32_pipe_peak(int device, int iters, int mode, double *ops_per_s, double *kernel_ms)
+{
+    if (mode != 0 && mode != 1)
+        return fail(SIMBA_EINVAL, "pipe probe mode must be 0 (ALU) or 1 (ALU + FMA), got %d", mode);
+    if (iters < 1)
+        return fail(SIMBA_EINVAL, "iters must be >= 1");
+    CK(cudaSetDevice(device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    uint32_t *d_out = nullptr;
+    CK(cudaMalloc(&d_out, sizeof(uint32_t)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = sms * 8, threads = 256;
+    auto launch = [&](uint32_t seed, int it) {
+        if (mode == 0)
+            int_pipe_kernel<0><<<blocks, threads>>>(seed, it, d_out);
+        else
+            int_pipe_kernel<1><<<blocks, threads>>>(seed, it, d_out);
+        g_launches++;
+    };
+    launch(12345u, 64);  // warm-up
+    CK(cudaEventRecord(e0));
+    launch(777u, iters);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaGetLastError());
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d_out);
+    *kernel_ms = ms;
+    *ops_per_s = (double)blocks * threads * (double)iters * 16.0 / (ms * 1e-3);
     return SIMBA_OK;
 }
 

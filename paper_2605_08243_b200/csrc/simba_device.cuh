@@ -93,6 +93,10 @@ struct KParams {
     unsigned long long *units;    // [0] units decoded, [1] units on the per-rank path
     unsigned int *flags;
     unsigned long long *planned;  // candidates queued so far (all CTAs): phase budgets
+    unsigned long long *dropped;  // lowest rank of a run dropped by the time budget
+    unsigned long long *xbest;    // shared minimum of a sharded search (another GPU's memory over
+                                  // NVLink, or this GPU's); null: none.  Hits are published to it,
+                                  // and claims and phases fold it into *best
     unsigned long long *pool;     // returned piece ranges (late splitting)          // bit 0: stopped by the time budget
     unsigned long long *stats;    // [2*path] calls, [2*path+1] candidates (SIMBA_STATS builds)
     void *queue;                  // tile descriptors, qcap per CTA (plan/execute phases)

@@ -294,6 +294,59 @@ class DeviceContext:
     def total(self, size: int) -> int:
         return self.table.total(size)
 
+    def set_shared_minimum(self, shared: "SharedMinimum | None") -> None:
+        """Attach (or, with None, detach) the shared minimum of a sharded
+        search: sharded SEARCH requests of this context publish their hits to
+        it and skip ranks above any shard's hit (simba_ctx_set_xbest)."""
+        N.check_rc(N.lib.simba_ctx_set_xbest(self._ptr, shared._ptr if shared is not None else None))
+        self._shared = shared  # the word must outlive the attachment
+
+
+class SharedMinimum:
+    """The 8-byte minimum (virtual rank) every shard of a sharded search
+    publishes its hits to and polls (SURVEY.md 8(e) early exit; simba_xbest).
+    Created on one process's GPU; the other processes open it from its CUDA
+    IPC handle (``handle``), over NVLink when their GPU differs."""
+
+    def __init__(self, device: int = 0, handle: bytes | None = None):
+        ptr = C.c_void_p()
+        if handle is None:
+            buf = (C.c_ubyte * N.XBEST_HANDLE_BYTES)()
+            N.check_rc(N.lib.simba_xbest_create(device, buf, C.byref(ptr)), "simba_xbest_create")
+            self.handle = bytes(buf)
+        else:
+            if len(handle) != N.XBEST_HANDLE_BYTES:
+                raise ValueError("shared-minimum handle must be 64 bytes")
+            buf = (C.c_ubyte * N.XBEST_HANDLE_BYTES).from_buffer_copy(handle)
+            N.check_rc(N.lib.simba_xbest_open(device, buf, C.byref(ptr)), "simba_xbest_open")
+            self.handle = bytes(handle)
+        self._ptr = ptr
+
+    def reset(self) -> None:
+        N.check_rc(N.lib.simba_xbest_reset(self._ptr))
+
+    def read(self) -> int | None:
+        v = C.c_uint64()
+        N.check_rc(N.lib.simba_xbest_read(self._ptr, C.byref(v)))
+        return None if v.value == N.NO_RANK else v.value
+
+    def close(self) -> None:
+        ptr = getattr(self, "_ptr", None)
+        if ptr:
+            self._ptr = None
+            lib = getattr(N, "lib", None)
+            if lib is not None:
+                lib.simba_xbest_destroy(ptr)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        self.close()
+
 
 def _check_args(spec: Specification, table: CountTable, cfg: EngineConfig):
     if spec.k != table.k:

@@ -12,6 +12,14 @@ GPUs, gloo in the CPU tests).  The result equals the single-device one:
 * search mode: a shard skips only ranks above its own best hit, so its result
   is the exact minimum of its shard and the MIN over shards is the level's
   minimum -- the (size, rank) the reference returns (engine.py:244-262).
+* early exit across GPUs (``search_fused(..., shared=...)``): the shards also
+  publish every hit to one shared 8-byte minimum (``SharedMinimum``: a word
+  on rank 0's GPU, mapped into the other ranks over NVLink by its CUDA IPC
+  handle) and fold it into their own bound at every claim and CTA phase, so
+  a shard stops claiming above ANY shard's hit -- the reference's break after
+  the first wave with a hit (engine.py:248-250).  Still exact: a chunk is
+  skipped only when its start is above a verified hit, which is >= the job's
+  minimum, so every chunk at or below the minimum is scanned by its owner.
 
 The device work is a ``scan(size, lo, hi, mode, shard, nshards, chunk)``
 callable (``DeviceContext.run`` on a GPU); the tests plug in the CPU oracle
@@ -95,10 +103,39 @@ def count_fused(scan_levels, size_bound: int, rank: int, world: int, device=None
                         int(sums[i, 1].item())) for i, (s, *_) in enumerate(levels)]
 
 
-def search_fused(scan_levels, size_bound: int, rank: int, world: int, device=None, group=None):
+def shared_minimum(rank: int, world: int, device: int = 0, group=None):
+    """One SharedMinimum for the job: created on rank 0's GPU, its IPC handle
+    broadcast once (the only setup exchange), opened by every other rank."""
+    import torch.distributed as dist
+
+    from .engine import SharedMinimum
+
+    obj = [None]
+    mine = None
+    if rank == 0:
+        mine = SharedMinimum(device)
+        obj[0] = mine.handle
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0, group=group)
+    if rank != 0:
+        mine = SharedMinimum(device, handle=obj[0])
+    return mine
+
+
+def search_fused(scan_levels, size_bound: int, rank: int, world: int, device=None, group=None, shared=None):
     """Algorithm 1 in one device request per rank: each shard returns its
     minimum (size, rank); the job's answer is the lexicographic minimum over
-    shards (MIN of the size, then MIN of the rank among shards at that size)."""
+    shards (MIN of the size, then MIN of the rank among shards at that size).
+    With `shared` (a SharedMinimum attached to every rank's context) the
+    shards stop above any shard's hit; rank 0 resets it and a barrier orders
+    the reset before every launch (the previous search's reductions already
+    ordered every launch before the reset)."""
+    if shared is not None and world > 1:
+        import torch.distributed as dist
+
+        if rank == 0:
+            shared.reset()
+        dist.barrier(group=group)
     r, levels = scan_levels(1, size_bound, "search", rank, world)
     size = r.size if r.best_rank is not None else None
     first = r.best_rank

@@ -83,9 +83,25 @@ def _worker(rank, world, port, cases, out):
                 fs, ff, _ = parallel.search_fused(oracle_levels(table, spec["k"], spec["w"], pairs, arg), C, rank,
                                                   world)
                 assert [fs, ff] == [size, first]
+                # with a shared minimum: rank 0 resets it, a barrier orders the reset
+                # before every rank's request (the device word is exercised in
+                # tests/test_xbest.py)
+                shared = _FakeShared()
+                fs, ff, _ = parallel.search_fused(oracle_levels(table, spec["k"], spec["w"], pairs, arg), C, rank,
+                                                  world, shared=shared)
+                assert [fs, ff] == [size, first]
+                assert shared.resets == (1 if rank == 0 else 0)
         out[rank] = res
     finally:
         dist.destroy_process_group()
+
+
+class _FakeShared:
+    def __init__(self):
+        self.resets = 0
+
+    def reset(self):
+        self.resets += 1
 
 
 @pytest.mark.parametrize("world", [2])

@@ -1,0 +1,140 @@
+"""Cross-GPU early exit of a sharded search (the reference's
+break after the first wave with a hit, engine.py:248-250): every shard
+publishes its hits to one shared 8-byte minimum (simba_xbest) and stops
+claiming above any shard's hit.  The answer must stay the exact minimum
+(size, rank) -- the oracle's and the single launch's -- while shards scan
+less.  The multi-process test maps the word into other processes through its
+CUDA IPC handle, as the ranks of a multi-GPU job do (here all on cuda:0)."""
+
+import os
+import random
+import socket
+
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+S = pytest.importorskip("paper_2605_08243_b200")
+from paper_2605_08243_b200 import _native as N  # noqa: E402
+from paper_2605_08243_b200 import codec, expr, parallel  # noqa: E402
+from paper_2605_08243_b200.engine import DeviceContext, SharedMinimum  # noqa: E402
+
+SIZE = 11
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_device():
+    if N.device_count() < 1:
+        pytest.fail("no CUDA device visible: the GPU tests must run on a B200")
+
+
+def planted(seed, target_size):
+    """k=4 w=32 n=10 spec labelled by a uniform expression of target_size."""
+    rng = random.Random(seed)
+    table = S.build(4, SIZE)
+    e = codec.sample_uniform(target_size, table, rng)
+    pairs, seen = [], set()
+    while len(pairs) < 10:
+        x = tuple(rng.getrandbits(32) for _ in range(4))
+        if x not in seen:
+            seen.add(x)
+            pairs.append((x, expr.evaluate(e, x, 32)))
+    return tuple(pairs)
+
+
+CASES = [(31, 9), (32, 10), (33, 10), (34, 11), (35, 11)]
+
+
+def oracle_answer(pairs, bound=SIZE):
+    tab = O.OracleTable(4, bound)
+    for s in range(1, bound + 1):
+        _, _, first, toks = O.scan_range(tab, 4, 32, list(pairs), s, 0, tab.total(s), 0, tab.total(s),
+                                         threads=O.cpu_count())
+        if first is not None:
+            return s, first, toks
+    return None, None, None
+
+
+def test_shared_minimum_in_process_exact_and_shorter():
+    for seed, ts in CASES:
+        pairs = tuple(planted(seed, ts))
+        spec = S.Specification(k=4, w=32, pairs=pairs)
+        want = oracle_answer(pairs)
+        assert want[0] is not None
+        table = S.build(4, SIZE)
+        vrank = sum(table.total(s) for s in range(1, want[0])) + want[1]
+        with DeviceContext(spec, SIZE) as ctx, SharedMinimum(0) as shared:
+            one, _ = ctx.run_levels(1, SIZE, mode="search")
+            assert (one.size, one.best_rank, one.tokens) == want
+            for nsh in (2, 8):
+                alone = [ctx.run_levels(1, SIZE, mode="search", shard=i, nshards=nsh)[0] for i in range(nsh)]
+                ctx.set_shared_minimum(shared)
+                shared.reset()
+                together = [ctx.run_levels(1, SIZE, mode="search", shard=i, nshards=nsh)[0] for i in range(nsh)]
+                ctx.set_shared_minimum(None)
+                for runs in (alone, together):
+                    hits = [(r.size, r.best_rank, r.tokens) for r in runs if r.best_rank is not None]
+                    assert min(hits) == want, (seed, nsh)
+                assert shared.read() == vrank
+                # later shards start from the published minimum: never more work
+                assert sum(r.visited for r in together) <= sum(r.visited for r in alone)
+                assert together[-1].visited <= alone[-1].visited
+
+
+def test_shared_minimum_detached_contexts_ignore_it():
+    pairs = tuple(planted(31, 9))
+    spec = S.Specification(k=4, w=32, pairs=pairs)
+    with DeviceContext(spec, SIZE) as ctx, SharedMinimum(0) as shared:
+        shared.reset()
+        # a single-shard or count request never touches the word
+        ctx.set_shared_minimum(shared)
+        ctx.run_levels(1, SIZE, mode="search")
+        ctx.run_levels(1, 9, mode="count", shard=0, nshards=2)
+        assert shared.read() is None
+        ctx.set_shared_minimum(None)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _rank_main(rank, world, port, cases, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shared = parallel.shared_minimum(rank, world, device=0)
+        res = []
+        for pairs in cases:
+            spec = S.Specification(k=4, w=32, pairs=tuple(pairs))
+            with DeviceContext(spec, SIZE, device=0) as ctx:
+                ctx.set_shared_minimum(shared)
+                size, first, levels = parallel.search_fused(parallel.device_levels(ctx), SIZE, rank, world,
+                                                            shared=shared)
+                ctx.set_shared_minimum(None)
+            res.append([size, first, sum(v for *_, v in levels)])
+        dist.barrier()  # the creator's word outlives every rank's searches
+        shared.close()
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shared_minimum_across_processes():
+    import torch.multiprocessing as mp
+
+    cases = [planted(seed, ts) for seed, ts in CASES]
+    want = [oracle_answer(p)[:2] for p in cases]
+    world = 3
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_rank_main, args=(world, _free_port(), cases, out), nprocs=world, join=True,
+                       start_method="spawn")
+    for rank in range(world):
+        got = out[rank]
+        assert [tuple(g[:2]) for g in got] == [tuple(w) for w in want], rank
