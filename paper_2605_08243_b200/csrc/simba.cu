@@ -16,6 +16,7 @@
 //                      on the first E examples), built once per context.
 //   decode_kernel      codec.decode of one rank (winner tokens).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges per launch and per synthesize level group
 
 #include <algorithm>
 #include <array>
@@ -62,6 +63,22 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+
+// NVTX range for the lifetime of a scope (no-op without a profiler attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *fmt, ...)
+    {
+        char buf[160];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        nvtxRangePushA(buf);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 int fail(int code, const char *fmt, ...)
 {
@@ -1703,6 +1720,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     od.R0 = min(od.s >= p.r0_up ? p.R0 + 1 : p.R0, od.s);
     od.lane = lane;
     od.ex = lane & (E - 1);
+    od.fine_end = 0;
     const bool early = (p.mode == SIMBA_MODE_SEARCH);
     const uint64_t t0 = globaltimer_ns();
     SweepStats ss{0, 0, 0};
@@ -1791,6 +1809,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                         if (early && c0 > read_best(p))
                             continue;  // ranks above a hit
                         od.reset();
+                        od.s = 0;  // re-derive the level's R0 (a piece may start in R0 mode)
                         n = c0;
                         have_piece = true;
                         continue;
@@ -1816,23 +1835,64 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                     break;
                 }
                 od.reset();
+                od.s = 0;
                 n = c0;
                 have_piece = true;
             }
             // the level holding n: pieces may cross level boundaries
             const int s = level_of(p, n);
+            const int cr0 = min(s >= p.r0_up ? p.R0 + 1 : p.R0, s);  // the level's R0
             if (s != od.s) {
                 od.s = s;
-                od.R0 = min(s >= p.r0_up ? p.R0 + 1 : p.R0, s);
+                od.R0 = cr0;
+                od.fine_end = 0;
                 od.reset();
             }
             const uint64_t vb = p.vbase[s];
             const uint64_t rn = n - vb;  // in-size rank
-            const uint64_t rend = min(c1, (uint64_t)p.vbase[s + 1]) - vb;
+            uint64_t rend = min(c1, (uint64_t)p.vbase[s + 1]) - vb;
+            if (od.fine_end) {  // a partial R0+1 row planned at R0
+                if (n >= od.fine_end) {
+                    od.fine_end = 0;
+                    od.R0 = cr0;
+                    od.reset();
+                } else {
+                    rend = min(rend, (uint64_t)(od.fine_end - vb));
+                }
+            }
             SIMBA_CYC_BEGIN(co);
             od.outer_at(rn);
             SIMBA_CYC_END(p, ST_CYC_OUTER, co);
-            const uint64_t pstop = min(od.pend, rend);
+            uint64_t pstop = min(od.pend, rend);
+            // Partial rows at R0 + 1 levels: a piece that starts or ends inside a
+            // row of T[R0+1] columns would leave a one-row tile (one G load per
+            // candidate, no reuse).  Plan such a partial row one digit finer
+            // instead (R0: rows of T[R0] columns, 2-D tiles again); the rank
+            // order and every candidate stay the same.
+            if (p.fine_row && od.R0 > p.R0 && !od.fine_end && !od.rs_valid && !od.ovf_o) {
+                const Tabs *t = stabs();
+                const uint64_t R2 = t->T[od.prsz];
+                if (R2 >= p.fine_row) {
+                    const uint64_t a = rn - od.pb, ra = a - div_T(t, od.prsz, a) * R2;  // position in its row
+                    uint64_t fe = 0;
+                    if (ra) {
+                        fe = min(pstop, rn - ra + R2);  // leading partial row
+                    } else if (pstop < od.pend) {
+                        const uint64_t len = pstop - rn, full = len - (len - div_T(t, od.prsz, len) * R2);
+                        if (full == 0)
+                            fe = pstop;  // only a trailing partial row is left
+                        else
+                            pstop = rn + full;  // full rows now, the trailing partial row next
+                    }
+                    if (fe) {
+                        od.fine_end = vb + fe;
+                        od.R0 = p.R0;
+                        od.reset();
+                        od.outer_at(rn);
+                        pstop = min(od.pend, fe);
+                    }
+                }
+            }
             uint64_t rn2;
             if (od.ovf_o) {
                 ++ss.units;
@@ -2216,6 +2276,8 @@ struct simba_ctx {
     int r0_up_env = 0;     // SIMBA_R0_UP override (diagnostics)
     uint32_t guide_env = 0;  // SIMBA_GUIDE override of the claim guide (diagnostics)
     uint64_t big_launch = 0;  // candidates per shard from which launches use the big shapes (SIMBA_BIG_LAUNCH)
+    uint64_t r0_rows = SIMBA_R0_ROWS;  // R0 + 1 needs first claims of this many rows (SIMBA_R0_ROWS env)
+    long long fine_row_env = -1;  // SIMBA_FINE_ROW override of KParams::fine_row (0: off; diagnostics)
     uint64_t last_super = 0;  // ranks per round-robin super-chunk of the last request
     uint64_t split_min = 0;  // pieces with at least this many ranks left split once claims run dry
     uint32_t tbl_len = 0, gtbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
@@ -2376,6 +2438,9 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
         return SIMBA_OK;
     CK(cudaSetDevice(c->device));
     const bool direct = rq.direct || rq.shuffled || c->kernel == 1;
+    NvtxRange nvtx_req("simba %s levels %d..%d [%llu,%llu) shard %llu/%llu%s", rq.mode == SIMBA_MODE_SEARCH ? "search" : "count",
+                       s_lo, rq.size, (unsigned long long)rq.lo, (unsigned long long)rq.hi,
+                       (unsigned long long)rq.shard, (unsigned long long)rq.nshards, rq.shuffled ? " shuffled" : "");
     const uint64_t range = rq.hi - rq.lo;
     const uint64_t warps = (uint64_t)(direct ? c->grid_direct : c->grid_unit) * (c->block_threads / 32);
     // chunk = claim granularity; super-chunk = sharding unit (round robin)
@@ -2423,7 +2488,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     // boundary, so the launch's first claims must span >= 16 such rows
     const uint64_t claim0 = per_shard / (warps * p.guide);
     p.r0_up = MAXS + 1;
-    if (c->r0_need && claim0 >= SIMBA_R0_ROWS * (c->r0_need >> SIMBA_R0_SHIFT)) {
+    if (c->r0_need && claim0 >= c->r0_rows * (c->r0_need >> SIMBA_R0_SHIFT)) {
         uint64_t vb = 0;  // virtual base of level s
         for (int s = 1; s <= rq.size; ++s) {
             const uint64_t T = row_total(c, s);
@@ -2442,6 +2507,8 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     if (c->guide_env)
         p.guide = c->guide_env;
     p.split_min = c->split_min;
+    // partial rows of size-(R0+1) super-leaves are planned at R0 (rows of T[R0])
+    p.fine_row = c->fine_row_env >= 0 ? (uint64_t)c->fine_row_env : row_total(c, c->R0) + 1;
     p.phase_guide = rq.nshards > 1 ? kShardPhaseGuide : kPhaseGuide;
     p.s_lo = s_lo;
     p.s_hi = rq.size;
@@ -2767,6 +2834,12 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->big_launch = kBigLaunch;
     if (const char *e = getenv("SIMBA_BIG_LAUNCH"))
         c->big_launch = strtoull(e, nullptr, 10);
+    c->r0_rows = SIMBA_R0_ROWS;
+    if (const char *e = getenv("SIMBA_R0_ROWS"))
+        c->r0_rows = strtoull(e, nullptr, 10);
+    c->fine_row_env = -1;
+    if (const char *e = getenv("SIMBA_FINE_ROW"))
+        c->fine_row_env = std::max(0LL, atoll(e));
     c->guide_env = 0;
     if (const char *e = getenv("SIMBA_GUIDE"))
         c->guide_env = (uint32_t)std::max(1, atoi(e));
@@ -3193,6 +3266,7 @@ int simba_synthesize(simba_ctx *c, int size_bound, int shuffled, double time_bud
             while (s_hi < size_bound && acc <= kFuseCands && row_total(c, s_hi + 1) <= kFuseCands - acc)
                 acc += row_total(c, ++s_hi);
             const auto t0 = clk::now();
+            NvtxRange nvtx_lv("synthesize levels %d..%d", s_lo, s_hi);
             std::vector<simba_level> lv(s_hi - s_lo + 1);
             simba_result r{};
             int rc = simba_run_levels(c, s_lo, s_hi, SIMBA_MODE_SEARCH, 0, 1,

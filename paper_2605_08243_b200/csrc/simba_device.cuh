@@ -107,6 +107,7 @@ struct KParams {
     // levels [s_lo, s_hi] of one launch in a virtual rank space: level s holds
     // virtual ranks [vbase[s], vbase[s + 1]); lo/hi/best/stop_above are virtual
     int s_lo, s_hi;
+    uint64_t fine_row;  // partial rows of at least this many columns at R0 + 1 levels are planned at R0 (0: off)
     const unsigned long long *vbase;  // [MAXS + 2] (global; kept out of the parameter block)
     unsigned long long *lvl;      // per level: [s] count, [MAXS+1+s] visited, [2*(MAXS+1)+s] first rank
 };
@@ -574,6 +575,7 @@ struct Odometer {
     uint32_t gen;          // bumped whenever the outer chain (so) is recomposed
     bool ovf_o, ovf_l;
     uint64_t phase_budget, phase_cands;  // candidates the warp may plan / has planned in this phase
+    uint64_t fine_end;     // != 0: planning a partial R0+1 row at R0 until this virtual rank
     // planner resume point inside a 2-D row group (queue filled mid-group)
     bool rs_valid;
     uint32_t rs_c;

@@ -102,14 +102,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank_main(rank, world, port, cases, out):
+def _rank_main(rank, world, port, cases, count_bound, out):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         shared = parallel.shared_minimum(rank, world, device=0)
-        res = []
+        res, counts = [], []
         for pairs in cases:
             spec = S.Specification(k=4, w=32, pairs=tuple(pairs))
             with DeviceContext(spec, SIZE, device=0) as ctx:
@@ -117,24 +117,42 @@ def _rank_main(rank, world, port, cases, out):
                 size, first, levels = parallel.search_fused(parallel.device_levels(ctx), SIZE, rank, world,
                                                             shared=shared)
                 ctx.set_shared_minimum(None)
+                lv = parallel.count_fused(parallel.device_levels(ctx), count_bound, rank, world)
             res.append([size, first, sum(v for *_, v in levels)])
+            counts.append([[x.size, x.count, x.first_rank, x.visited] for x in lv])
         dist.barrier()  # the creator's word outlives every rank's searches
         shared.close()
-        out[rank] = res
+        out[rank] = (res, counts)
     finally:
         dist.destroy_process_group()
 
 
-def test_shared_minimum_across_processes():
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world", [3, 8])
+def test_sharded_device_path_across_processes(world):
+    """The multi-GPU protocol with the real device path: `world` processes
+    (gloo; all on cuda:0 here, one GPU each on a multi-GPU node) shard the
+    fused search with the shared minimum and the fused count; every rank gets
+    the oracle's (size, rank) and the oracle's per-level counts."""
     import torch.multiprocessing as mp
 
     cases = [planted(seed, ts) for seed, ts in CASES]
     want = [oracle_answer(p)[:2] for p in cases]
-    world = 3
+    count_bound = 10
+    tab = O.OracleTable(4, count_bound)
+    want_counts = []
+    for p in cases:
+        rows = []
+        for s in range(1, count_bound + 1):
+            _, c, f, _ = O.scan_range(tab, 4, 32, list(p), s, 0, tab.total(s), 0, tab.total(s),
+                                      threads=O.cpu_count())
+            rows.append([s, c, f, tab.total(s)])
+        want_counts.append(rows)
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.start_processes(_rank_main, args=(world, _free_port(), cases, out), nprocs=world, join=True,
+    mp.start_processes(_rank_main, args=(world, _free_port(), cases, count_bound, out), nprocs=world, join=True,
                        start_method="spawn")
     for rank in range(world):
-        got = out[rank]
+        got, counts = out[rank]
         assert [tuple(g[:2]) for g in got] == [tuple(w) for w in want], rank
+        assert counts == want_counts, rank
