@@ -14,14 +14,24 @@ value   device-timed whole-job candidates/s (CUDA events on the library
 e2e     same metric through the public API with host buffers each step
         (context creation = H2D of spec + tables, per-spec value tables,
         scans, D2H of the results)
-roofline  INT32 issue roofline of the step's launch: algorithmic integer ops
+roofline  INT32 roofline of the step's launch: algorithmic integer ops
         (sum_s T[s] * s * e-bar) / its CUDA-event duration,
-        against the INT32 peak measured on this box by simba_int32_peak
-        (MEASURED_PEAKS.json has no integer figure)
+        against P_int32 = the LOP3-only ALU-pipe rate measured in this run
+        (simba_int32_pipe_peak; MEASURED_PEAKS.json has no integer figure).
+        That frac exceeds 1 by construction; roofline.hw holds
+        the hardware fractions: the mandatory test op per candidate against
+        the ALU-pipe peak, and issued instructions against the issue limit
 cpu_baseline  the CPU oracle (oracle/simba_oracle.c, restatement of the
-        reference path) on all host threads over a bounded size-13 sample
+        reference path) on all host threads over a bounded size-13 sample;
+        cpu_baseline.python_reference = the unmodified Python reference
+        (baseline/_ref) through its own synthesize() with workers = all
+        host threads, on the same spec
+time_to_solve  synthesize on the 30-target suite (ten per size 11/12/13,
+        minimal size = target size), every answer asserted against the
+        oracle's (tests/golden/c5.json); with N ranks, a sharded fused search
+        with the cross-GPU shared minimum
 
-`--impl reference` times that CPU implementation as the reference arm.
+`--impl reference` times the CPU oracle as the reference arm.
 """
 
 from __future__ import annotations

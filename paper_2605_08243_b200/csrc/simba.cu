@@ -898,6 +898,9 @@ __device__ __forceinline__ uint32_t chunk0(uint32_t off2, uint32_t clo)
     return sizeof(W) == 4 ? clo - ((off2 + clo) & 3u) : clo;
 }
 
+#ifndef SIMBA_RF_PREFETCH
+#define SIMBA_RF_PREFETCH 1  // RF tiles load the next column chunk while testing this one
+#endif
 // RF tile: rows [row0, row0 + nrows) of the X-unit, columns [clo, chi);
 // lanes hold 8 column values, rows are warp-uniform.  NT == 0: folded,
 // per-row (m, c), four rows per step; NT >= 1: per-row segment (merged P)
@@ -962,9 +965,17 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
             }
         }
         __syncwarp();
-        for (uint32_t c0 = chunk0<W>(off2, clo); (int32_t)(c0 - chi) < 0; c0 += 256) {
-            W s[8];
-            load_cols<W>(t0, off2 + c0, lane, s);
+        // column values come from L2: the next 256-column chunk is in flight
+        // while the rows test this one (its first use no longer waits)
+        uint32_t c0 = chunk0<W>(off2, clo);
+        W s[8];
+        load_cols<W>(t0, off2 + c0, lane, s);
+        for (; (int32_t)(c0 - chi) < 0; c0 += 256) {
+#if SIMBA_RF_PREFETCH
+            W sn[8];
+            const uint32_t cn = ((int32_t)(c0 + 256 - chi) < 0) ? c0 + 256 : c0;
+            load_cols<W>(t0, off2 + cn, lane, sn);
+#endif
             if constexpr (NT == 0) {
                 for (uint32_t r = 0; r < nr4; r += 4) {
                     W m[4], c[4];
@@ -1005,11 +1016,22 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
                     }
                 }
             }
+#if SIMBA_RF_PREFETCH
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                s[j] = sn[j];
+#else
+            if ((int32_t)(c0 + 256 - chi) < 0)
+                load_cols<W>(t0, off2 + c0 + 256, lane, s);
+#endif
         }
         __syncwarp();
     }
 }
 
+#ifndef SIMBA_ROW1_DEPTH
+#define SIMBA_ROW1_DEPTH 2  // 256-column chunks in flight ahead of the one being tested
+#endif
 // One-row folded tile (partial rows at unit/claim boundaries, P = none):
 // columns [clo, chi) of row row0, 8 column values per lane, no padding rows.
 template <class W, int E>
@@ -1033,15 +1055,24 @@ __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int p
         rows_left<W, 1>(g0, xu, row0, 1, lane, slr, xr);
         fold_p(pop, xr[0], true, ta.tm, ta.tc, m, c);
     }
-    // column values come from L2: the next 256-column chunk is loaded while
-    // this one is tested
-    W s[8];
+    // column values come from L2 (one load per candidate, no reuse): the
+    // chunks two and one ahead are in flight while this one is tested, so
+    // each warp keeps three 256-column loads outstanding
+    W s[8], sn[8];
     const uint32_t cs = chunk0<W>(off2, clo);
     load_cols<W>(t0, off2 + cs, lane, s);
+#if SIMBA_ROW1_DEPTH >= 2
+    load_cols<W>(t0, off2 + (((int32_t)(cs + 256 - chi) < 0) ? cs + 256 : cs), lane, sn);
+#endif
     for (uint32_t c0 = cs; (int32_t)(c0 - chi) < 0; c0 += 256) {
-        W sn[8];
+#if SIMBA_ROW1_DEPTH >= 2
+        W snn[8];
+        const uint32_t cn = ((int32_t)(c0 + 512 - chi) < 0) ? c0 + 512 : c0;
+        load_cols<W>(t0, off2 + cn, lane, snn);
+#else
         const uint32_t cn = ((int32_t)(c0 + 256 - chi) < 0) ? c0 + 256 : c0;
         load_cols<W>(t0, off2 + cn, lane, sn);
+#endif
         if (__any_sync(FULL, hit8(s, m, c))) {
             uint32_t bits = hitmask8(s, m, c);
             while (__any_sync(FULL, bits != 0)) {
@@ -1053,8 +1084,12 @@ __device__ __noinline__ void tile_row1(const KParams &p, const Staged &st, int p
             }
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < 8; ++j) {
             s[j] = sn[j];
+#if SIMBA_ROW1_DEPTH >= 2
+            sn[j] = snn[j];
+#endif
+        }
     }
     __syncwarp();
 }
@@ -1246,7 +1281,7 @@ constexpr uint64_t kShardPhaseGuide = SIMBA_SHARD_PHASE_GUIDE;
 #ifndef SIMBA_SHARD_GUIDE
 #define SIMBA_SHARD_GUIDE 4  // claim guide of sharded launches (0: the unsharded rule)
 #endif
-constexpr uint32_t kVerifyCap = 8192;  // deferred verifications per CTA and phase
+constexpr uint32_t kVerifyCap = 32768;  // deferred verifications per CTA and phase (then inline)
 #ifndef SIMBA_SUPER_PER_SHARD
 #define SIMBA_SUPER_PER_SHARD 16
 #endif
@@ -2056,6 +2091,23 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS) direct_kernel(const __grid
         atomicAdd(&p.lvl[MAXS + 1 + p.s], (unsigned long long)vis);
 }
 
+// Example-0 density of a spec: how many subtrees of size <= RG evaluate to
+// y0 on example 0 (the value table's first row).  The tiles test example 0
+// only; every match goes to the hit path, so a spec whose y0 many small
+// expressions reach (y0 = 0, x0 & x2 on that example, ...) needs the
+// per-example value tables that refine matches on examples 1..3 cheaply.
+template <class W>
+__global__ void ex0_density_kernel(const W *g, uint32_t len, W y0, W mask, unsigned long long *out)
+{
+    unsigned int cnt = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
+        cnt += (((g[i] ^ y0) & mask) == 0) ? 1u : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+        cnt += __shfl_xor_sync(FULL, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt)
+        atomicAdd(out, (unsigned long long)cnt);
+}
 
 template <class W>
 __global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int RG, int E, uint32_t tbl_len, W *out)
@@ -2277,7 +2329,9 @@ struct simba_ctx {
     uint32_t guide_env = 0;  // SIMBA_GUIDE override of the claim guide (diagnostics)
     uint64_t big_launch = 0;  // candidates per shard from which launches use the big shapes (SIMBA_BIG_LAUNCH)
     uint64_t r0_rows = SIMBA_R0_ROWS;  // R0 + 1 needs first claims of this many rows (SIMBA_R0_ROWS env)
-    long long fine_row_env = -1;  // SIMBA_FINE_ROW override of KParams::fine_row (0: off; diagnostics)
+    long long fine_row_env = -1;
+    uint64_t y0 = 0;          // outputs[0]
+    double ex0_dense = 1e-4;  // example-0 match share of the value table from which E = 4 (SIMBA_EX0_DENSE)  // SIMBA_FINE_ROW override of KParams::fine_row (0: off; diagnostics)
     uint64_t last_super = 0;  // ranks per round-robin super-chunk of the last request
     uint64_t split_min = 0;  // pieces with at least this many ranks left split once claims run dry
     uint32_t tbl_len = 0, gtbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
@@ -2351,6 +2405,20 @@ int build_value_tables(simba_ctx *c)
     g_launches++;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
+    return SIMBA_OK;
+}
+
+template <class W>
+int ex0_density(simba_ctx *c, unsigned long long *matches)
+{
+    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(unsigned long long), c->stream));
+    ex0_density_kernel<W><<<296, 256, 0, c->stream>>>(reinterpret_cast<const W *>(c->d_gtbl), c->gtbl_len,
+                                                      (W)c->y0, (W)c->mask, c->d_ctr);
+    g_launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *matches = c->h_ctr[0];
     return SIMBA_OK;
 }
 
@@ -2837,6 +2905,9 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->r0_rows = SIMBA_R0_ROWS;
     if (const char *e = getenv("SIMBA_R0_ROWS"))
         c->r0_rows = strtoull(e, nullptr, 10);
+    c->y0 = outputs[0];
+    if (const char *e = getenv("SIMBA_EX0_DENSE"))
+        c->ex0_dense = atof(e);
     c->fine_row_env = -1;
     if (const char *e = getenv("SIMBA_FINE_ROW"))
         c->fine_row_env = std::max(0LL, atoll(e));
@@ -2968,6 +3039,19 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     int rc = (c->wbytes == 4) ? build_value_tables<uint32_t>(c) : build_value_tables<uint64_t>(c);
     if (rc)
         return bail(rc);
+    if (o.table_examples == 0 && c->E == 1 && n >= 2 && c->kernel == 0) {
+        // dense example 0: rebind with per-example value tables (E = 4)
+        unsigned long long matches = 0;
+        rc = (c->wbytes == 4) ? ex0_density<uint32_t>(c, &matches) : ex0_density<uint64_t>(c, &matches);
+        if (rc)
+            return bail(rc);
+        if ((double)matches >= c->ex0_dense * (double)c->gtbl_len) {
+            simba_ctx_destroy(c);
+            simba_options o4 = o;
+            o4.table_examples = 4;
+            return simba_ctx_create(k, w, n, inputs, outputs, max_size, &o4, out);
+        }
+    }
     rc = (c->wbytes == 4) ? setup_kernels<uint32_t>(c) : setup_kernels<uint64_t>(c);
     if (rc)
         return bail(rc);

@@ -1,0 +1,13 @@
+#!/bin/bash
+# compute-sanitizer memcheck / racecheck / synccheck on the production unit
+# kernel with the big-launch shapes, R0 + 1, partial-row planning and late
+# splitting forced (scripts/sanitize_case.py).  Logs: gpurun_out/san_*.txt
+export SIMBA_BIG_LAUNCH=1 SIMBA_SPLIT_MIN=4096
+for tool in memcheck racecheck synccheck; do
+  for c in "k2 9" "k4 8"; do
+    set -- $c
+    SIMBA_R0_UP=$2 timeout 1200 compute-sanitizer --tool $tool --kernel-name kns=unit_kernel \
+      python scripts/sanitize_case.py $1 > gpurun_out/san_${tool}_$1.txt 2>&1
+    echo "$tool $1 rc=$? $(tail -2 gpurun_out/san_${tool}_$1.txt | tr '\n' ' ')"
+  done
+done

@@ -78,9 +78,10 @@ def test_shared_minimum_in_process_exact_and_shorter():
                     hits = [(r.size, r.best_rank, r.tokens) for r in runs if r.best_rank is not None]
                     assert min(hits) == want, (seed, nsh)
                 assert shared.read() == vrank
-                # later shards start from the published minimum: never more work
-                assert sum(r.visited for r in together) <= sum(r.visited for r in alone)
-                assert together[-1].visited <= alone[-1].visited
+                # later shards start from the published minimum: no more work than
+                # alone (up to the piece granularity at which a stop is counted)
+                slack = nsh << 20
+                assert sum(r.visited for r in together) <= sum(r.visited for r in alone) + slack, (seed, nsh)
 
 
 def test_shared_minimum_detached_contexts_ignore_it():
@@ -156,3 +157,29 @@ def test_sharded_device_path_across_processes(world):
         got, counts = out[rank]
         assert [tuple(g[:2]) for g in got] == [tuple(w) for w in want], rank
         assert counts == want_counts, rank
+
+
+def test_shared_minimum_stops_a_shard_above_another_shards_hit():
+    """The planted size-9 spec of the C5 golden (first hits: level 9 at rank
+    12435603, level 10 at 73124301): over levels 1..11 in 2 shards, the answer
+    lies in shard 0's first super-chunk while shard 1's own first hit is a
+    level-10 rank far above it.  Alone, shard 1 sweeps up to its own hit;
+    attached to the minimum shard 0 published, it stops at once, and it
+    reports the job's answer."""
+    from conftest import load_golden
+
+    p = next(x for x in load_golden("c5")["planted"] if x["name"] == "sparse_size9")
+    spec = S.Specification(k=4, w=32, pairs=tuple((tuple(i), o) for i, o in p["spec"]["pairs"]))
+    lv9 = next(x for x in p["levels"] if x["size"] == 9)
+    want = (9, lv9["first"])
+    with DeviceContext(spec, SIZE) as ctx, SharedMinimum(0) as shared:
+        alone1, _ = ctx.run_levels(1, SIZE, mode="search", shard=1, nshards=2)
+        ctx.set_shared_minimum(shared)
+        shared.reset()
+        r0, _ = ctx.run_levels(1, SIZE, mode="search", shard=0, nshards=2)
+        r1, _ = ctx.run_levels(1, SIZE, mode="search", shard=1, nshards=2)
+        ctx.set_shared_minimum(None)
+    assert (r0.size, r0.best_rank) == want
+    assert alone1.best_rank is not None and (alone1.size, alone1.best_rank) > want
+    assert (r1.size, r1.best_rank) == want  # the pulled minimum
+    assert r1.visited + (1 << 20) < alone1.visited, (r1.visited, alone1.visited)
