@@ -28,6 +28,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "simba_device.cuh"
@@ -898,6 +899,22 @@ __device__ __forceinline__ uint32_t chunk0(uint32_t off2, uint32_t clo)
     return sizeof(W) == 4 ? clo - ((off2 + clo) & 3u) : clo;
 }
 
+#ifndef SIMBA_GEN_AFFINE
+#define SIMBA_GEN_AFFINE 1  // GEN tiles of an arithmetic P: first segment as one IMAD
+#endif
+__device__ __forceinline__ bool pop_arith(int pop) { return pop == OP_ADD || pop == OP_SUB || pop == OP_MUL; }
+
+// first segment of a GEN candidate: AFF = the segment has no bitwise part
+// (m = ~0, x = 0), so it is a * v + b
+template <class W, bool AFF>
+__device__ __forceinline__ W seg_first(const Seg<W> &g, W v)
+{
+    if constexpr (AFF)
+        return g.a * v + g.b;
+    else
+        return seg_apply(g, v);
+}
+
 #ifndef SIMBA_RF_PREFETCH
 #define SIMBA_RF_PREFETCH 1  // RF tiles load the next column chunk while testing this one
 #endif
@@ -992,29 +1009,38 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
                     }
                 }
             } else {
-                for (uint32_t r = 0; r < nr; ++r) {
-                    const Seg<W> g = buf[r];
-                    W v[8];
+                // an arithmetic P's row segment has no bitwise part (pseg_left;
+                // gen_merges merges only bitwise-free residuals into it): one
+                // IMAD per candidate instead of LOP3 + IMAD
+                auto gen_rows = [&](auto aff) {
+                    for (uint32_t r = 0; r < nr; ++r) {
+                        const Seg<W> g = buf[r];
+                        W v[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        W u = seg_apply(g, s[j]);
+                        for (int j = 0; j < 8; ++j) {
+                            W u = seg_first<W, decltype(aff)::value>(g, s[j]);
 #pragma unroll
-                        for (int i = 0; i < NT - 1; ++i)
-                            u = seg_apply(res[i], u);
-                        v[j] = u;
-                    }
-                    if (__any_sync(FULL, hit8(v, TM, TC))) {
-                        uint32_t bits = hitmask8(v, TM, TC);
-                        while (__any_sync(FULL, bits != 0)) {
-                            SIMBA_WD("rf1-slow", bits, c0);
-                            const int b = bits ? __ffs(bits) - 1 : 0;
-                            const uint32_t d2 = c0 + col_off<W>(lane, b);
-                            const bool h = bits != 0 && d2 - clo < chi - clo;
-                            bits &= bits - 1;
-                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, d2, my_count);
+                            for (int i = 0; i < NT - 1; ++i)
+                                u = seg_apply(res[i], u);
+                            v[j] = u;
+                        }
+                        if (__any_sync(FULL, hit8(v, TM, TC))) {
+                            uint32_t bits = hitmask8(v, TM, TC);
+                            while (__any_sync(FULL, bits != 0)) {
+                                SIMBA_WD("rf1-slow", bits, c0);
+                                const int b = bits ? __ffs(bits) - 1 : 0;
+                                const uint32_t d2 = c0 + col_off<W>(lane, b);
+                                const bool h = bits != 0 && d2 - clo < chi - clo;
+                                bits &= bits - 1;
+                                on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, d2, my_count);
+                            }
                         }
                     }
-                }
+                };
+                if (SIMBA_GEN_AFFINE && pop_arith(pop))
+                    gen_rows(std::true_type{});
+                else
+                    gen_rows(std::false_type{});
             }
 #if SIMBA_RF_PREFETCH
 #pragma unroll
@@ -1165,28 +1191,34 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop
                 }
             }
         } else {
-            for (uint32_t cc = 0; cc < R2; ++cc) {
-                const Seg<W> g = buf[cc];
-                W v[NJ];
+            auto gen_cols = [&](auto aff) {  // see tile_rf: arithmetic P, one IMAD per candidate
+                for (uint32_t cc = 0; cc < R2; ++cc) {
+                    const Seg<W> g = buf[cc];
+                    W v[NJ];
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    W u = seg_apply(g, x[j]);
+                    for (int j = 0; j < NJ; ++j) {
+                        W u = seg_first<W, decltype(aff)::value>(g, x[j]);
 #pragma unroll
-                    for (int i = 0; i < NT - 1; ++i)
-                        u = seg_apply(res[i], u);
-                    v[j] = u;
-                }
-                if (__any_sync(FULL, hitN<W, NJ>(v, TM, TC))) {
-                    uint32_t bits = hitmaskN<W, NJ>(v, TM, TC);
-                    while (__any_sync(FULL, bits != 0)) {
-                        const int b = bits ? __ffs(bits) - 1 : 0;
-                        const uint32_t r = lane + 32 * b;
-                        const bool h = bits != 0 && r < nb;
-                        bits &= bits - 1;
-                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc, my_count);
+                        for (int i = 0; i < NT - 1; ++i)
+                            u = seg_apply(res[i], u);
+                        v[j] = u;
+                    }
+                    if (__any_sync(FULL, hitN<W, NJ>(v, TM, TC))) {
+                        uint32_t bits = hitmaskN<W, NJ>(v, TM, TC);
+                        while (__any_sync(FULL, bits != 0)) {
+                            const int b = bits ? __ffs(bits) - 1 : 0;
+                            const uint32_t r = lane + 32 * b;
+                            const bool h = bits != 0 && r < nb;
+                            bits &= bits - 1;
+                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r, cc, my_count);
+                        }
                     }
                 }
-            }
+            };
+            if (SIMBA_GEN_AFFINE && pop_arith(pop))
+                gen_cols(std::true_type{});
+            else
+                gen_cols(std::false_type{});
         }
     }
     __syncwarp();
@@ -1659,6 +1691,9 @@ __device__ __forceinline__ bool pool_pop(const KParams &p, uint64_t &a, uint64_t
 // kBigLaunch candidates (fewer, longer claims: fewer rows cut at claim
 // boundaries), twice that below (shorter tails when the launch is short)
 constexpr uint32_t kGuideBig = SIMBA_GUIDE;
+#ifndef SIMBA_FUSED_GUIDE
+#define SIMBA_FUSED_GUIDE 2  // big multi-level launches (the C5 sweep): 19.75 -> 19.3 ms; a single level stays at 4
+#endif
 #ifndef SIMBA_BIG_LAUNCH
 #define SIMBA_BIG_LAUNCH 40000000000ull
 #endif
@@ -2408,6 +2443,41 @@ int build_value_tables(simba_ctx *c)
     return SIMBA_OK;
 }
 
+// Keep the global value table resident in L2: rows and columns are read from
+// it at random (X values of sizes <= RG) throughout every launch, and without
+// a persisting window the 80 MB table (k=4, RG=9) is read from HBM about 20
+// times per C5 sweep.  Best effort: a device without persisting L2 (or a
+// window smaller than the table) keeps the hit ratio the window allows.
+// SIMBA_L2_PERSIST=0 turns it off (A/B).
+void l2_persist(simba_ctx *c)
+{
+    if (const char *e = getenv("SIMBA_L2_PERSIST"))
+        if (atoi(e) == 0)
+            return;
+    int max_persist = 0, max_window = 0;
+    if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device) != cudaSuccess ||
+        max_persist <= 0 || max_window <= 0) {
+        cudaGetLastError();
+        return;
+    }
+    const size_t bytes = ((size_t)c->E * c->gtbl_len + kTblPad) * c->wbytes;
+    const size_t win = std::min(bytes, (size_t)max_window);
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur < std::min(win, (size_t)max_persist))
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(win, (size_t)max_persist));
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.base_ptr = c->d_gtbl;
+    a.accessPolicyWindow.num_bytes = win;
+    a.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)cur / (double)win);
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &a);
+    cudaGetLastError();  // best effort
+}
+
 template <class W>
 int ex0_density(simba_ctx *c, unsigned long long *matches)
 {
@@ -2547,7 +2617,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     // use R0 + 1; large launches use larger descriptors and claims
     const uint64_t per_shard = range / rq.nshards;
     p.desc_cands = per_shard >= c->big_launch ? kDescCandsBig : kDescCandsBig / 2;
-    p.guide = per_shard >= c->big_launch ? kGuideBig : 2 * kGuideBig;
+    p.guide = per_shard >= c->big_launch ? (s_lo < rq.size ? SIMBA_FUSED_GUIDE : kGuideBig) : 2 * kGuideBig;
 #if SIMBA_SHARD_GUIDE
     if (rq.nshards > 1)
         p.guide = SIMBA_SHARD_GUIDE;
@@ -3055,6 +3125,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     rc = (c->wbytes == 4) ? setup_kernels<uint32_t>(c) : setup_kernels<uint64_t>(c);
     if (rc)
         return bail(rc);
+    l2_persist(c);
     {
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
