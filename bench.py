@@ -446,11 +446,16 @@ def int_peaks(N, device):
 
 
 def lib_sha16():
+    """Identity of the libsimba build: sha256 of its CUDA sources and header
+    (what a rebuild with the same nvcc reproduces; the binary itself is not
+    byte-stable across rebuilds)."""
     import hashlib
 
-    from paper_2605_08243_b200 import _native as N
-
-    return hashlib.sha256(Path(N.LIB_PATH).read_bytes()).hexdigest()[:16]
+    h = hashlib.sha256()
+    for f in ("paper_2605_08243_b200/csrc/simba.cu", "paper_2605_08243_b200/csrc/simba_device.cuh",
+              "paper_2605_08243_b200/csrc/vfb_impl.cuh", "include/simba.h"):
+        h.update((ROOT / f).read_bytes())
+    return h.hexdigest()[:16]
 
 
 def profile_summary(sha):

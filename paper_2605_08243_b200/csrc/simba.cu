@@ -609,11 +609,14 @@ __device__ __forceinline__ uint32_t div_T32(const Tabs *t, int sz, uint32_t n)
 // example 0.  Rows past `cnt` repeat the last row (callers mask them); all
 // loads are issued before any is used (skipping unneeded 32-row groups with
 // uniform branches measured slower: it serialises the loads).
+// Row values of X-unit rows d0 + lane + 32 j (j < NJ, clamped to cnt - 1),
+// in two stages so that a caller can issue the next batch's loads before it
+// uses this one: rows_load issues the G loads (both table digits when X is
+// N_X(Y, L1), else L1), rows_finish combines them and applies LEFT.
 template <class W, int NJ>
-__device__ __forceinline__ void rows_left(const W *g0, const XU &xu, uint64_t d0, uint32_t cnt, int lane,
-                                          const Seg<W> (&sl)[MAXSL], W (&x)[NJ])
+__device__ __forceinline__ void rows_load(const W *g0, const XU &xu, uint64_t d0, uint32_t cnt, int lane,
+                                          W (&a)[NJ], W (&b)[NJ])
 {
-    W in[NJ];
     if (xu.x2d) {
         // rows d0 + o, o < 256: dy = dy0 + (rem0 + o) / R1p (R1p = T[sz1] < 2^27)
         const Tabs *t = stabs();
@@ -621,7 +624,6 @@ __device__ __forceinline__ void rows_left(const W *g0, const XU &xu, uint64_t d0
         const uint32_t rem0 = (uint32_t)(d0 - dy0 * xu.R1p);
         const W *gy = g0 + xu.offy + dy0;
         const W *g1 = g0 + xu.off1;
-        W a[NJ], b[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             const uint32_t r = rem0 + min((uint32_t)lane + 32u * j, cnt - 1);
@@ -629,6 +631,22 @@ __device__ __forceinline__ void rows_left(const W *g0, const XU &xu, uint64_t d0
             a[j] = __ldg(gy + q);
             b[j] = __ldg(g1 + (r - q * (uint32_t)xu.R1p));
         }
+    } else {
+        const W *g = g0 + xu.off1 + d0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            a[j] = __ldg(g + min((uint32_t)lane + 32u * j, cnt - 1));
+            b[j] = (W)0;
+        }
+    }
+}
+
+template <class W, int NJ>
+__device__ __forceinline__ void rows_finish(const XU &xu, const Seg<W> (&sl)[MAXSL], const W (&a)[NJ],
+                                            const W (&b)[NJ], W (&x)[NJ])
+{
+    W in[NJ];
+    if (xu.x2d) {
         switch (xu.pxop) {
         case OP_AND:
 #pragma unroll
@@ -656,14 +674,22 @@ __device__ __forceinline__ void rows_left(const W *g0, const XU &xu, uint64_t d0
             break;
         }
     } else {
-        const W *g = g0 + xu.off1 + d0;
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
-            in[j] = __ldg(g + min((uint32_t)lane + 32u * j, cnt - 1));
+            in[j] = a[j];
     }
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
         x[j] = segs_apply(sl, in[j]);
+}
+
+template <class W, int NJ>
+__device__ __forceinline__ void rows_left(const W *g0, const XU &xu, uint64_t d0, uint32_t cnt, int lane,
+                                          const Seg<W> (&sl)[MAXSL], W (&x)[NJ])
+{
+    W a[NJ], b[NJ];
+    rows_load<W, NJ>(g0, xu, d0, cnt, lane, a, b);
+    rows_finish<W, NJ>(xu, sl, a, b, x);
 }
 
 // P as a segment on the variable operand (GEN tiles): f fixed on the left
@@ -915,6 +941,9 @@ __device__ __forceinline__ W seg_first(const Seg<W> &g, W v)
         return seg_apply(g, v);
 }
 
+#ifndef SIMBA_CF_PREFETCH
+#define SIMBA_CF_PREFETCH 1  // CF tiles issue the next row batch's loads before testing this one
+#endif
 #ifndef SIMBA_RF_PREFETCH
 #define SIMBA_RF_PREFETCH 1  // RF tiles load the next column chunk while testing this one
 #endif
@@ -1170,10 +1199,22 @@ __device__ __noinline__ void tile_cf(const KParams &p, const Staged &st, int pop
         }
     }
     __syncwarp();
+#if SIMBA_CF_PREFETCH
+    // the next row batch's G loads are in flight while this batch is tested
+    W ra[NJ], rb_[NJ];
+    rows_load<W, NJ>(g0, xu, row0, (uint32_t)min((uint64_t)(32 * NJ), nrows), lane, ra, rb_);
+#endif
     for (uint64_t rb = 0; rb < nrows; rb += 32 * NJ) {
         const uint32_t nb = (uint32_t)min((uint64_t)(32 * NJ), nrows - rb);
         W x[NJ];
+#if SIMBA_CF_PREFETCH
+        rows_finish<W, NJ>(xu, slr, ra, rb_, x);  // rows past nb are masked at hit time
+        if (rb + 32 * NJ < nrows)
+            rows_load<W, NJ>(g0, xu, row0 + rb + 32 * NJ,
+                             (uint32_t)min((uint64_t)(32 * NJ), nrows - rb - 32 * NJ), lane, ra, rb_);
+#else
         rows_left<W, NJ>(g0, xu, row0 + rb, nb, lane, slr, x);  // rows past nb are masked at hit time
+#endif
         if constexpr (NT == 0) {
             for (uint32_t cc = 0; cc < R4; cc += 4) {
                 W m[4], c[4];
