@@ -1279,6 +1279,8 @@ __device__ __forceinline__ void dispatch_rf(const KParams &p, const Staged &st, 
                                             uint64_t nrows, uint32_t clo, uint32_t chi, int lane, uint64_t &cnt)
 {
     SIMBA_STAT(p, nrows == 1 ? ST_RF_ROW : nt == 0 ? ST_RF_FOLD : ST_RF_GEN, nrows * (chi - clo));
+    if (pop == OP_NONE)
+        SIMBA_STAT(p, ST_ROW_NONE, nrows * (chi - clo));
     SIMBA_CYC_BEGIN(ct);
     if (nt == 0 && nrows == 1)
         tile_row1<W, E>(p, st, pop, xu, ubase, R2, off2, row0, clo, chi, lane, cnt);
@@ -1832,6 +1834,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     od.lane = lane;
     od.ex = lane & (E - 1);
     od.fine_end = 0;
+    od.absorb = p.absorb != 0;
     const bool early = (p.mode == SIMBA_MODE_SEARCH);
     const uint64_t t0 = globaltimer_ns();
     SweepStats ss{0, 0, 0};
@@ -1957,6 +1960,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                 od.s = s;
                 od.R0 = cr0;
                 od.fine_end = 0;
+                od.absorb = p.absorb != 0;
                 od.reset();
             }
             const uint64_t vb = p.vbase[s];
@@ -1966,6 +1970,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                 if (n >= od.fine_end) {
                     od.fine_end = 0;
                     od.R0 = cr0;
+                    od.absorb = p.absorb != 0;
                     od.reset();
                 } else {
                     rend = min(rend, (uint64_t)(od.fine_end - vb));
@@ -1980,7 +1985,8 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             // candidate, no reuse).  Plan such a partial row one digit finer
             // instead (R0: rows of T[R0] columns, 2-D tiles again); the rank
             // order and every candidate stay the same.
-            if (p.fine_row && od.R0 > p.R0 && !od.fine_end && !od.rs_valid && !od.ovf_o) {
+            if (p.fine_row && !od.fine_end && !od.rs_valid && !od.ovf_o &&
+                (od.R0 > p.R0 || (od.pop != OP_NONE && od.prsz > od.R0))) {
                 const Tabs *t = stabs();
                 const uint64_t R2 = t->T[od.prsz];
                 if (R2 >= p.fine_row) {
@@ -1998,6 +2004,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                     if (fe) {
                         od.fine_end = vb + fe;
                         od.R0 = p.R0;
+                        od.absorb = false;  // (it would take the coarse node as P again)
                         od.reset();
                         od.outer_at(rn);
                         pstop = min(od.pend, fe);
@@ -2406,6 +2413,7 @@ struct simba_ctx {
     uint64_t big_launch = 0;  // candidates per shard from which launches use the big shapes (SIMBA_BIG_LAUNCH)
     uint64_t r0_rows = SIMBA_R0_ROWS;  // R0 + 1 needs first claims of this many rows (SIMBA_R0_ROWS env)
     long long fine_row_env = -1;
+    int absorb = 1;  // unary-topped right children of size R0+1 absorbed into P blocks (SIMBA_ABSORB=0: off)
     uint64_t y0 = 0;          // outputs[0]
     double ex0_dense = 1e-4;  // example-0 match share of the value table from which E = 4 (SIMBA_EX0_DENSE)  // SIMBA_FINE_ROW override of KParams::fine_row (0: off; diagnostics)
     uint64_t last_super = 0;  // ranks per round-robin super-chunk of the last request
@@ -2688,6 +2696,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.split_min = c->split_min;
     // partial rows of size-(R0+1) super-leaves are planned at R0 (rows of T[R0])
     p.fine_row = c->fine_row_env >= 0 ? (uint64_t)c->fine_row_env : row_total(c, c->R0) + 1;
+    p.absorb = c->absorb;
     p.phase_guide = rq.nshards > 1 ? kShardPhaseGuide : kPhaseGuide;
     p.s_lo = s_lo;
     p.s_hi = rq.size;
@@ -3019,6 +3028,9 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->y0 = outputs[0];
     if (const char *e = getenv("SIMBA_EX0_DENSE"))
         c->ex0_dense = atof(e);
+    c->absorb = 1;
+    if (const char *e = getenv("SIMBA_ABSORB"))
+        c->absorb = atoi(e) != 0;
     c->fine_row_env = -1;
     if (const char *e = getenv("SIMBA_FINE_ROW"))
         c->fine_row_env = std::max(0LL, atoll(e));

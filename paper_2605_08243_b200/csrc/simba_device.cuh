@@ -24,6 +24,7 @@ enum : int {
     ST_DIRECT,
     ST_PH_PLAN, ST_PH_EXEC, ST_PH_VERIFY,  // (phases, CTA cycles) of each phase (thread 0)
     ST_W_PLAN, ST_W_EXEC,                 // (warp phases, warp busy cycles) inside plan / exec
+    ST_ROW_NONE,                          // one-row tiles of a P-less region (a unary node above L2)
     ST_N
 };
 #ifdef SIMBA_STATS
@@ -108,6 +109,7 @@ struct KParams {
     // virtual ranks [vbase[s], vbase[s + 1]); lo/hi/best/stop_above are virtual
     int s_lo, s_hi;
     uint64_t fine_row;  // partial rows of at least this many columns at R0 + 1 levels are planned at R0 (0: off)
+    int absorb;         // Odometer::absorb (SIMBA_ABSORB)
     const unsigned long long *vbase;  // [MAXS + 2] (global; kept out of the parameter block)
     unsigned long long *lvl;      // per level: [s] count, [MAXS+1+s] visited, [2*(MAXS+1)+s] first rank
 };
@@ -576,6 +578,7 @@ struct Odometer {
     bool ovf_o, ovf_l;
     uint64_t phase_budget, phase_cands;  // candidates the warp may plan / has planned in this phase
     uint64_t fine_end;     // != 0: planning a partial R0+1 row at R0 until this virtual rank
+    bool absorb;           // a binary node whose right child (size R0+1) starts with NOT/NEG is P
     // planner resume point inside a 2-D row group (queue filled mid-group)
     bool rs_valid;
     uint32_t rs_c;
@@ -663,7 +666,18 @@ struct Odometer {
             const int rsz = sz - 1 - j;
             const uint64_t q = div_T(t, rsz, r);
             const uint64_t rr = r - q * t->T[rsz];
-            if (rsz <= R0) {
+            // A right child of size R0 + 1 that is NOT/NEG of a size-R0 subtree would
+            // end the walk below it with no P: every X row of this node becomes a
+            // one-row region (tile_row1, one G load per candidate).  Take this node
+            // as P instead, with rows of T[R0+1] columns from the value table: the
+            // same ranks, tiled 2-D.
+            bool take = rsz <= R0;
+            if (!take && absorb && rsz == R0 + 1 && rsz <= RG) {
+                uint64_t r2 = rr;
+                const int op2 = find_slot(t, rsz, r2);
+                take = (op2 == OP_NOT || op2 == OP_NEG);
+            }
+            if (take) {
                 pop = op;
                 pj = j;
                 prsz = rsz;

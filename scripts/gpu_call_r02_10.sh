@@ -1,0 +1,4 @@
+echo "== stats"; SIMBA_LIB=$PWD/paper_2605_08243_b200/_lib/libsimba_stats.so timeout 300 python scripts/probe_shard_stats.py
+for i in 1 2; do for lib in libsimba.so libsimba_dpw32.so libsimba_desc19.so; do
+  echo "== $lib"; SIMBA_LIB=$PWD/paper_2605_08243_b200/_lib/$lib timeout 300 python scripts/probe_shapes.py 0:0
+done; done
