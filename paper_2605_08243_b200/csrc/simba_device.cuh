@@ -554,6 +554,10 @@ struct WarpLevels {
     int cur_s;              // level of the tile being executed (hit path)
 };
 
+#ifndef SIMBA_ABSORB_MAX
+#define SIMBA_ABSORB_MAX 1  // absorbed right children: sizes R0 + 1 .. R0 + SIMBA_ABSORB_MAX (2: sweep 19.5 vs 18.1 ms)
+#endif
+
 template <class W, int E>
 struct Odometer {
     WarpLevels<W, E> *L;   // this warp's shared-memory levels
@@ -666,16 +670,26 @@ struct Odometer {
             const int rsz = sz - 1 - j;
             const uint64_t q = div_T(t, rsz, r);
             const uint64_t rr = r - q * t->T[rsz];
-            // A right child of size R0 + 1 that is NOT/NEG of a size-R0 subtree would
-            // end the walk below it with no P: every X row of this node becomes a
-            // one-row region (tile_row1, one G load per candidate).  Take this node
-            // as P instead, with rows of T[R0+1] columns from the value table: the
-            // same ranks, tiled 2-D.
+            // A right child whose own walk would pass only NOT/NEG nodes on its way
+            // down to size <= R0 (NOT(z), NEG(NOT(z)), ...) ends with no P: every X
+            // row of this node becomes a one-row region (tile_row1, one G load per
+            // candidate).  Take this node as P instead, with rows of T[rsz]
+            // columns from the value table (rsz <= R0 + SIMBA_ABSORB_MAX, <= RG):
+            // the same ranks, tiled 2-D.
             bool take = rsz <= R0;
-            if (!take && absorb && rsz == R0 + 1 && rsz <= RG) {
+            if (!take && absorb && rsz <= R0 + SIMBA_ABSORB_MAX && rsz <= RG) {
                 uint64_t r2 = rr;
-                const int op2 = find_slot(t, rsz, r2);
-                take = (op2 == OP_NOT || op2 == OP_NEG);
+                int sz2 = rsz;
+                take = true;
+                while (sz2 > R0) {
+                    const int op2 = find_slot(t, sz2, r2);
+                    if (op2 == OP_NOT || op2 == OP_NEG) {
+                        --sz2;  // r2 is now the rank inside the unary's child
+                        continue;
+                    }
+                    take = false;  // a binary node: the walk finds a P (or goes on) below
+                    break;
+                }
             }
             if (take) {
                 pop = op;
