@@ -2192,6 +2192,41 @@ __global__ void ex0_density_kernel(const W *g, uint32_t len, W y0, W mask, unsig
         atomicAdd(out, (unsigned long long)cnt);
 }
 
+// Value table level `sz`, built bottom-up from the levels below it: entry r of
+// size sz is its top operator applied to one or two table entries of smaller
+// sizes -- the first step of decode_into (codec.py:108-130) and one operation
+// of eval_tokens, in the same full word width (so the values equal
+// value_table_kernel's decode + eval_rpn per entry, at a fraction of the work).
+template <class W>
+__global__ void value_level_kernel(const Tabs *tabs, const W *X, int k, int sz, int E, uint32_t tbl_len, W *out)
+{
+    const uint32_t n = (uint32_t)tabs->T[sz];
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (uint32_t)E * n)
+        return;
+    const uint32_t e = idx / n, r = idx - e * n;
+    W *g = out + (size_t)e * tbl_len;
+    W v;
+    if (sz == 1) {
+        v = X[(size_t)e * k + r];
+    } else {
+        uint64_t rr = r;
+        const int op = find_slot(tabs, sz, rr);
+        if (op == OP_NOT || op == OP_NEG) {
+            const W a = g[tabs->toff[sz - 1] + (uint32_t)rr];
+            v = (op == OP_NOT) ? (W)~a : (W)((W)0 - a);
+        } else {
+            const int j = find_split(tabs, sz, rr);
+            const int rsz = sz - 1 - j;
+            const uint64_t q = rr / tabs->T[rsz];
+            const W a = g[tabs->toff[j] + (uint32_t)q];
+            const W b = g[tabs->toff[rsz] + (uint32_t)(rr - q * tabs->T[rsz])];
+            v = apply_bin<W>(op, a, b);
+        }
+    }
+    g[tabs->toff[sz] + r] = v;
+}
+
 template <class W>
 __global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int RG, int E, uint32_t tbl_len, W *out)
 {
@@ -2415,6 +2450,7 @@ struct simba_ctx {
     long long fine_row_env = -1;
     int absorb = 1;  // unary-topped right children of size R0+1 absorbed into P blocks (SIMBA_ABSORB=0: off)
     uint64_t y0 = 0;          // outputs[0]
+    bool value_tables_by_decode = false;  // SIMBA_VT_DECODE=1: per-entry decode + eval (the cross-check)
     double ex0_dense = 1e-4;  // example-0 match share of the value table from which E = 4 (SIMBA_EX0_DENSE)  // SIMBA_FINE_ROW override of KParams::fine_row (0: off; diagnostics)
     uint64_t last_super = 0;  // ranks per round-robin super-chunk of the last request
     uint64_t split_min = 0;  // pieces with at least this many ranks left split once claims run dry
@@ -2481,13 +2517,24 @@ int setup_kernels(simba_ctx *c)
 template <class W>
 int build_value_tables(simba_ctx *c)
 {
-    const uint32_t total = (uint32_t)c->E * c->gtbl_len;
-    const int bt = 128;
-    value_table_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(
-        c->d_tabs, reinterpret_cast<const W *>(c->d_blob + c->tbl_bytes), c->k, c->RG, c->E, c->gtbl_len,
-        reinterpret_cast<W *>(c->d_gtbl));
-    g_launches++;
-    CK(cudaGetLastError());
+    const int bt = 256;
+    const W *X = reinterpret_cast<const W *>(c->d_blob + c->tbl_bytes);
+    W *G = reinterpret_cast<W *>(c->d_gtbl);
+    if (c->value_tables_by_decode) {  // reference-exact decode + eval per entry (SIMBA_VT_DECODE=1; tests)
+        const uint32_t total = (uint32_t)c->E * c->gtbl_len;
+        value_table_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(c->d_tabs, X, c->k, c->RG, c->E,
+                                                                            c->gtbl_len, G);
+        g_launches++;
+        CK(cudaGetLastError());
+    } else {  // bottom-up, one launch per size (each level reads only the ones below)
+        for (int sz = 1; sz <= c->RG; ++sz) {
+            const uint32_t total = (uint32_t)c->E * (uint32_t)c->h_tabs.T[sz];
+            value_level_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(c->d_tabs, X, c->k, sz, c->E,
+                                                                              c->gtbl_len, G);
+            g_launches++;
+            CK(cudaGetLastError());
+        }
+    }
     CK(cudaStreamSynchronize(c->stream));
     return SIMBA_OK;
 }
@@ -3026,6 +3073,8 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     if (const char *e = getenv("SIMBA_R0_ROWS"))
         c->r0_rows = strtoull(e, nullptr, 10);
     c->y0 = outputs[0];
+    if (const char *e = getenv("SIMBA_VT_DECODE"))
+        c->value_tables_by_decode = atoi(e) != 0;
     if (const char *e = getenv("SIMBA_EX0_DENSE"))
         c->ex0_dense = atof(e);
     c->absorb = 1;

@@ -188,3 +188,17 @@ def test_c5_time_to_solve_suite_matches_oracle():
             assert out.size == int(size)
             n += 1
     assert n == sum(len(v) for v in g["tts"].values()) > 0
+
+
+@pytest.mark.parametrize("name", ["k3_w4", "k4_w32_x0px1"])
+def test_value_tables_bottom_up_equal_per_entry_decode(name, monkeypatch):
+    """The value tables are built bottom-up (one operator per entry over the
+    levels below); SIMBA_VT_DECODE=1 builds them by the reference-exact
+    per-entry decode + eval instead.  Both give the oracle's counts."""
+    sp, C, _ = DENSE[name]
+    want = oracle_levels(name)
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SIMBA_VT_DECODE", mode)
+        with DeviceContext(spec_of(sp), C) as ctx:
+            _, levels = ctx.run_levels(1, C, mode="count")
+        assert [tuple(x) for x in levels] == want, mode
