@@ -941,6 +941,9 @@ __device__ __forceinline__ W seg_first(const Seg<W> &g, W v)
         return seg_apply(g, v);
 }
 
+#ifndef SIMBA_RF_ROWS8
+#define SIMBA_RF_ROWS8 1  // RF folded tiles test 8 rows per step
+#endif
 #ifndef SIMBA_CF_PREFETCH
 #define SIMBA_CF_PREFETCH 1  // CF tiles issue the next row batch's loads before testing this one
 #endif
@@ -1023,19 +1026,38 @@ __device__ __noinline__ void tile_rf(const KParams &p, const Staged &st, int pop
             load_cols<W>(t0, off2 + cn, lane, sn);
 #endif
             if constexpr (NT == 0) {
-                for (uint32_t r = 0; r < nr4; r += 4) {
+                // the slow path of one 4-row group (hits on example 0 present)
+                auto group_hits = [&](uint32_t r, const W (&m)[4], const W (&c)[4]) {
+                    uint32_t bits = hitmask8x4(s, m, c);
+                    while (__any_sync(FULL, bits != 0)) {
+                        const int b = bits ? __ffs(bits) - 1 : 0;
+                        const uint32_t k = b >> 3, d2 = c0 + col_off<W>(lane, b & 7);
+                        const bool h = bits != 0 && r + k < nr && d2 - clo < chi - clo;
+                        bits &= bits - 1;
+                        on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r + k, d2, my_count);
+                    }
+                };
+                uint32_t r = 0;
+#if SIMBA_RF_ROWS8
+                // 8 rows per step: 8 independent predicate chains, one vote
+                for (; r + 8 <= nr4; r += 8) {
+                    W m[4], c[4], m2[4], c2[4];
+                    load4(pb + r, m, c);
+                    load4(pb + r + 4, m2, c2);
+                    const bool h1 = hit8x4(s, m, c), h2 = hit8x4(s, m2, c2);
+                    if (__any_sync(FULL, h1 || h2)) {
+                        if (__any_sync(FULL, h1))
+                            group_hits(r, m, c);
+                        if (__any_sync(FULL, h2))
+                            group_hits(r + 4, m2, c2);
+                    }
+                }
+#endif
+                for (; r < nr4; r += 4) {
                     W m[4], c[4];
                     load4(pb + r, m, c);
-                    if (__any_sync(FULL, hit8x4(s, m, c))) {
-                        uint32_t bits = hitmask8x4(s, m, c);
-                        while (__any_sync(FULL, bits != 0)) {
-                            const int b = bits ? __ffs(bits) - 1 : 0;
-                            const uint32_t k = b >> 3, d2 = c0 + col_off<W>(lane, b & 7);
-                            const bool h = bits != 0 && r + k < nr && d2 - clo < chi - clo;
-                            bits &= bits - 1;
-                            on_hits<W, E>(p, st, sx, pop, xu, ubase, R2, off2, h, row0 + rb + r + k, d2, my_count);
-                        }
-                    }
+                    if (__any_sync(FULL, hit8x4(s, m, c)))
+                        group_hits(r, m, c);
                 }
             } else {
                 // an arithmetic P's row segment has no bitwise part (pseg_left;
