@@ -1374,6 +1374,7 @@ constexpr int kDescPerWarp = SIMBA_DPW;
 #define SIMBA_SHARD_PHASE_GUIDE 1  // sharded launches (nshards > 1): 8-way shards 4.47 -> 4.22 ms
 #endif
 constexpr uint64_t kPhaseGuide = SIMBA_PHASE_GUIDE;  // phase budget ~ remaining / (warps * guide)
+
 constexpr uint64_t kShardPhaseGuide = SIMBA_SHARD_PHASE_GUIDE;
 #ifndef SIMBA_SHARD_GUIDE
 #define SIMBA_SHARD_GUIDE 4  // claim guide of sharded launches (0: the unsharded rule)
@@ -1689,7 +1690,7 @@ struct Claim {
 // they finish.  A pusher always returns to the pool before exiting, so every
 // pushed range is taken.  Slot state: 0 empty, 1 full, 2/3 being written/read.
 #ifndef SIMBA_SPLIT_MIN_LOG2
-#define SIMBA_SPLIT_MIN_LOG2 19
+#define SIMBA_SPLIT_MIN_LOG2 17  // 2^19: sweep mean 19.1-19.4 ms over 40 launches, 2^17: 18.6-18.9
 #endif
 constexpr uint64_t kSplitMin = SIMBA_SPLIT_MIN_LOG2 ? 1ull << SIMBA_SPLIT_MIN_LOG2 : 0;  // 0: no splitting
 
