@@ -2471,6 +2471,7 @@ struct simba_ctx {
     uint64_t big_launch = 0;  // candidates per shard from which launches use the big shapes (SIMBA_BIG_LAUNCH)
     uint64_t r0_rows = SIMBA_R0_ROWS;  // R0 + 1 needs first claims of this many rows (SIMBA_R0_ROWS env)
     long long fine_row_env = -1;
+    uint64_t super_per_shard = kSuperPerShard;  // SIMBA_SUPER_PER_SHARD env
     int absorb = 1;  // unary-topped right children of size R0+1 absorbed into P blocks (SIMBA_ABSORB=0: off)
     uint64_t y0 = 0;          // outputs[0]
     bool value_tables_by_decode = false;  // SIMBA_VT_DECODE=1: per-entry decode + eval (the cross-check)
@@ -2712,7 +2713,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
             chunk <<= 1;
         spc = 1;
         if (rq.nshards > 1) {
-            const uint64_t per = range / (rq.nshards * kSuperPerShard) + 1;  // super-chunks per shard
+            const uint64_t per = range / (rq.nshards * c->super_per_shard) + 1;  // super-chunks per shard
             while (spc * chunk < per && spc < (1ull << 20))
                 spc <<= 1;
         } else {
@@ -3100,6 +3101,9 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         c->value_tables_by_decode = atoi(e) != 0;
     if (const char *e = getenv("SIMBA_EX0_DENSE"))
         c->ex0_dense = atof(e);
+    c->super_per_shard = kSuperPerShard;
+    if (const char *e = getenv("SIMBA_SUPER_PER_SHARD"))
+        c->super_per_shard = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
     c->absorb = 1;
     if (const char *e = getenv("SIMBA_ABSORB"))
         c->absorb = atoi(e) != 0;
