@@ -1367,6 +1367,9 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 #define SIMBA_DESC_LOG2 18
 #endif
 constexpr int kDescPerWarp = SIMBA_DPW;
+#ifndef SIMBA_FUSED_DPW
+#define SIMBA_FUSED_DPW 16
+#endif
 #ifndef SIMBA_PHASE_GUIDE
 #define SIMBA_PHASE_GUIDE 0  // unsharded launches: 0 = no phase budget (measured best for single launches)
 #endif
@@ -1484,7 +1487,7 @@ __device__ __forceinline__ void emit_tile(const KParams &p, Odometer<W, E> &od, 
     // once spent, the warp stops planning for this phase
     od.phase_cands += cands;
     if (od.phase_cands >= od.phase_budget)
-        emitted = max(emitted, kDescPerWarp);
+        emitted = max(emitted, (int)p.dpw);
 }
 
 // One descriptor: stage its chains in the warp's shared block, run the tile.
@@ -1930,7 +1933,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             if (__shfl_sync(FULL, pushed, 0))
                 c1 = n + (c1 - n) / 2;
         }
-        while (!done && emitted < kDescPerWarp) {
+        while (!done && emitted < (int)p.dpw) {
             SIMBA_WD("plan", n, emitted);
             if (!have_piece) {
                 if (!have_claim || v >= cl.v1) {
@@ -2041,7 +2044,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                 direct_range<W>(p, st, rn, pstop, false, ss.count, s);
                 rn2 = pstop;
             } else {
-                rn2 = plan_pblock<W, E>(p, st, od, rn, pstop, lane, ss, emitted, kDescPerWarp);
+                rn2 = plan_pblock<W, E>(p, st, od, rn, pstop, lane, ss, emitted, (int)p.dpw);
             }
             n = vb + rn2;
             if (n >= c1 || (early && n > read_best(p))) {  // piece finished (or the rest ranks above a hit)
@@ -2472,6 +2475,7 @@ struct simba_ctx {
     uint64_t r0_rows = SIMBA_R0_ROWS;  // R0 + 1 needs first claims of this many rows (SIMBA_R0_ROWS env)
     long long fine_row_env = -1;
     uint64_t super_per_shard = kSuperPerShard;  // SIMBA_SUPER_PER_SHARD env
+    uint32_t dpw_env = 0;  // SIMBA_DPW_RT: descriptors per warp and phase (<= SIMBA_DPW; diagnostics)
     int absorb = 1;  // unary-topped right children of size R0+1 absorbed into P blocks (SIMBA_ABSORB=0: off)
     uint64_t y0 = 0;          // outputs[0]
     bool value_tables_by_decode = false;  // SIMBA_VT_DECODE=1: per-entry decode + eval (the cross-check)
@@ -2769,6 +2773,12 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.fine_row = c->fine_row_env >= 0 ? (uint64_t)c->fine_row_env : row_total(c, c->R0) + 1;
     p.absorb = c->absorb;
     p.phase_guide = rq.nshards > 1 ? kShardPhaseGuide : kPhaseGuide;
+    // descriptors per warp and phase: fewer in big fused (multi-level) launches,
+    // whose last full phases set the launch's end (the bench sweep: mean of 60
+    // launches 18.9 -> 18.25 ms at 16); single levels and shards keep 24
+    p.dpw = (rq.nshards == 1 && s_lo < rq.size && per_shard >= c->big_launch) ? SIMBA_FUSED_DPW : kDescPerWarp;
+    if (c->dpw_env)
+        p.dpw = std::min<uint32_t>(c->dpw_env, kDescPerWarp);
     p.s_lo = s_lo;
     p.s_hi = rq.size;
     p.vbase = c->d_lvl + kLvlWords;  // the level bases follow the per-level counters
@@ -3104,6 +3114,9 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->super_per_shard = kSuperPerShard;
     if (const char *e = getenv("SIMBA_SUPER_PER_SHARD"))
         c->super_per_shard = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
+    c->dpw_env = 0;
+    if (const char *e = getenv("SIMBA_DPW_RT"))
+        c->dpw_env = (uint32_t)std::max(1, atoi(e));
     c->absorb = 1;
     if (const char *e = getenv("SIMBA_ABSORB"))
         c->absorb = atoi(e) != 0;

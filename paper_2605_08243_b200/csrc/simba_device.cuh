@@ -102,6 +102,7 @@ struct KParams {
     unsigned long long *stats;    // [2*path] calls, [2*path+1] candidates (SIMBA_STATS builds)
     void *queue;                  // tile descriptors, qcap per CTA (plan/execute phases)
     uint32_t qcap;
+    uint32_t dpw;                 // descriptors per warp and phase (<= kDescPerWarp)
     uint32_t ps_off;              // shared-memory offset of the CTA's queue bookkeeping
     unsigned long long *vq;       // deferred verification queue, vqcap ranks per CTA (null: verify inline)
     uint32_t vqcap;

@@ -202,3 +202,30 @@ def test_value_tables_bottom_up_equal_per_entry_decode(name, monkeypatch):
         with DeviceContext(spec_of(sp), C) as ctx:
             _, levels = ctx.run_levels(1, C, mode="count")
         assert [tuple(x) for x in levels] == want, mode
+
+
+@pytest.mark.parametrize("mode", ["local", "shuffled"])
+def test_budget_never_reports_a_non_minimal_hit(mode):
+    """Under a time budget a run dropped by the budget records its lowest rank;
+    a hit above a dropped run is not reported (the reference, scanning chunks
+    in order, would have timed out before it, engine.py:251-258), and in
+    shuffled order a cut-short block reports no hit.  So every FOUND equals
+    the oracle's minimum, whatever the budget -- checked over budgets from
+    0 to well past the search time on a spec with hits at many ranks."""
+    sp, C, _ = DENSE["k4_w32_x0px1"]
+    want = oracle_levels("k4_w32_x0px1")
+    first = next((s, f) for s, c, f, _ in want if c)
+    # a spec whose first hit sits deep in a large level: the pieces below it
+    # are what a budget can drop
+    spec = spec_of(sp)
+    table = S.build(4, C)
+    seen = set()
+    for budget in (0.0, 1e-5, 3e-5, 1e-4, 3e-4, 1e-3, 1.0):
+        for _ in range(3):
+            out = S.synthesize(spec, table, S.EngineConfig(size_bound=C, mode=mode, time_budget=budget))
+            seen.add(out.status)
+            if out.status is S.Status.FOUND:
+                assert (out.size, out.rank) == first, (budget, mode)
+            else:
+                assert out.status is S.Status.TIMED_OUT and out.expr is None
+    assert S.Status.FOUND in seen
