@@ -2603,11 +2603,11 @@ void l2_persist(simba_ctx *c)
 }
 
 template <class W>
-int ex0_density(simba_ctx *c, unsigned long long *matches)
+int ex0_density(simba_ctx *c, unsigned long long *matches, int e = 0, uint64_t y = 0)
 {
     CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(unsigned long long), c->stream));
-    ex0_density_kernel<W><<<296, 256, 0, c->stream>>>(reinterpret_cast<const W *>(c->d_gtbl), c->gtbl_len,
-                                                      (W)c->y0, (W)c->mask, c->d_ctr);
+    ex0_density_kernel<W><<<296, 256, 0, c->stream>>>(reinterpret_cast<const W *>(c->d_gtbl) + (size_t)e * c->gtbl_len,
+                                                      c->gtbl_len, (W)(e ? y : c->y0), (W)c->mask, c->d_ctr);
     g_launches++;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
@@ -3256,17 +3256,75 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     unsigned __int128 cum = 0;
     for (int z = 1; z <= max_size; ++z)
         cum += c->rows[z][8];
-    if (o.table_examples == 0 && c->E == 1 && n >= 2 && c->kernel == 0 && cum >= ((unsigned __int128)1 << 30)) {
-        // dense example 0: rebind with per-example value tables (E = 4)
-        unsigned long long matches = 0;
-        rc = (c->wbytes == 4) ? ex0_density<uint32_t>(c, &matches) : ex0_density<uint64_t>(c, &matches);
-        if (rc)
-            return bail(rc);
-        if ((double)matches >= c->ex0_dense * (double)c->gtbl_len) {
-            simba_ctx_destroy(c);
-            simba_options o4 = o;
-            o4.table_examples = 4;
-            return simba_ctx_create(k, w, n, inputs, outputs, max_size, &o4, out);
+    if (o.table_examples == 0 && n >= 2 && c->kernel == 0 && cum >= ((unsigned __int128)1 << 30)) {
+        simba_ctx *c4 = nullptr;
+        if (c->E == 1) {
+            // dense example 0: rebind with per-example value tables (E = 4)
+            unsigned long long matches = 0;
+            rc = (c->wbytes == 4) ? ex0_density<uint32_t>(c, &matches) : ex0_density<uint64_t>(c, &matches);
+            if (rc)
+                return bail(rc);
+            if ((double)matches >= c->ex0_dense * (double)c->gtbl_len) {
+                simba_ctx_destroy(c);
+                simba_options o4 = o;
+                o4.table_examples = 4;
+                rc = simba_ctx_create(k, w, n, inputs, outputs, max_size, &o4, &c4);
+                if (rc)
+                    return rc;
+                c = nullptr;
+            }
+        } else {
+            // per-example tables chosen by the low-entropy rule: finish this
+            // context first (setup below), then check the primary example
+            c4 = nullptr;
+        }
+        if (c4 || c->E > 1) {
+            simba_ctx *ce = c4 ? c4 : c;
+            if (!c4) {
+                rc = (ce->wbytes == 4) ? setup_kernels<uint32_t>(ce) : setup_kernels<uint64_t>(ce);
+                if (rc)
+                    return bail(rc);
+                l2_persist(ce);
+                int sms = 0;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ce->device);
+                if (o.blocks_per_sm > 0) {
+                    ce->grid_unit = std::min(ce->grid_unit, sms * o.blocks_per_sm);
+                    ce->grid_direct = std::min(ce->grid_direct, sms * o.blocks_per_sm);
+                }
+                ce->grid_unit = std::min(ce->grid_unit, sms * 2);
+            }
+            // The tiles test one example; make it the sparsest of those with
+            // tables (y0 = 0 on one example: 2% of all expressions match it,
+            // and every match takes the slow hit path).  The order of the
+            // examples does not change which candidates satisfy all of them.
+            int best = 0;
+            unsigned long long bm = ~0ull;
+            for (int e = 0; e < ce->E; ++e) {
+                unsigned long long m = 0;
+                rc = (ce->wbytes == 4) ? ex0_density<uint32_t>(ce, &m, e, outputs[e])
+                                       : ex0_density<uint64_t>(ce, &m, e, outputs[e]);
+                if (rc) {
+                    simba_ctx_destroy(ce);
+                    return rc;
+                }
+                if (m < bm) {
+                    bm = m;
+                    best = e;
+                }
+            }
+            if (best == 0) {
+                *out = ce;
+                return SIMBA_OK;
+            }
+            const int E = ce->E;
+            simba_ctx_destroy(ce);
+            std::vector<uint64_t> xin(inputs, inputs + (size_t)n * k), yout(outputs, outputs + n);
+            for (int j = 0; j < k; ++j)
+                std::swap(xin[j], xin[(size_t)best * k + j]);
+            std::swap(yout[0], yout[best]);
+            simba_options oe = o;
+            oe.table_examples = E;
+            return simba_ctx_create(k, w, n, xin.data(), yout.data(), max_size, &oe, out);
         }
     }
     rc = (c->wbytes == 4) ? setup_kernels<uint32_t>(c) : setup_kernels<uint64_t>(c);
