@@ -2476,6 +2476,8 @@ struct simba_ctx {
     long long fine_row_env = -1;
     uint64_t super_per_shard = kSuperPerShard;  // SIMBA_SUPER_PER_SHARD env
     uint32_t dpw_env = 0;  // SIMBA_DPW_RT: descriptors per warp and phase (<= SIMBA_DPW; diagnostics)
+    int shard_pg_env = -1;     // SIMBA_SHARD_PG: phase guide of sharded launches (diagnostics)
+    uint32_t shard_dpw_env = 0;  // SIMBA_SHARD_DPW: descriptors per warp and phase of sharded launches
     int absorb = 1;  // unary-topped right children of size R0+1 absorbed into P blocks (SIMBA_ABSORB=0: off)
     uint64_t y0 = 0;          // outputs[0]
     bool value_tables_by_decode = false;  // SIMBA_VT_DECODE=1: per-entry decode + eval (the cross-check)
@@ -2779,6 +2781,10 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.dpw = (rq.nshards == 1 && s_lo < rq.size && per_shard >= c->big_launch) ? SIMBA_FUSED_DPW : kDescPerWarp;
     if (c->dpw_env)
         p.dpw = std::min<uint32_t>(c->dpw_env, kDescPerWarp);
+    if (rq.nshards > 1 && c->shard_pg_env >= 0)
+        p.phase_guide = (uint64_t)c->shard_pg_env;
+    if (rq.nshards > 1 && c->shard_dpw_env)
+        p.dpw = std::min<uint32_t>(c->shard_dpw_env, kDescPerWarp);
     p.s_lo = s_lo;
     p.s_hi = rq.size;
     p.vbase = c->d_lvl + kLvlWords;  // the level bases follow the per-level counters
@@ -3114,6 +3120,12 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->super_per_shard = kSuperPerShard;
     if (const char *e = getenv("SIMBA_SUPER_PER_SHARD"))
         c->super_per_shard = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
+    c->shard_pg_env = -1;
+    if (const char *e = getenv("SIMBA_SHARD_PG"))
+        c->shard_pg_env = std::max(0, atoi(e));
+    c->shard_dpw_env = 0;
+    if (const char *e = getenv("SIMBA_SHARD_DPW"))
+        c->shard_dpw_env = (uint32_t)std::max(1, atoi(e));
     c->dpw_env = 0;
     if (const char *e = getenv("SIMBA_DPW_RT"))
         c->dpw_env = (uint32_t)std::max(1, atoi(e));
