@@ -1367,8 +1367,11 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 #define SIMBA_DESC_LOG2 18
 #endif
 constexpr int kDescPerWarp = SIMBA_DPW;
+#ifndef SIMBA_FUSED_DPW_LATE
+#define SIMBA_FUSED_DPW_LATE 16  // big fused launches once 3/4 of the chunks are claimed
+#endif
 #ifndef SIMBA_FUSED_DPW
-#define SIMBA_FUSED_DPW 16
+#define SIMBA_FUSED_DPW 24
 #endif
 #ifndef SIMBA_PHASE_GUIDE
 #define SIMBA_PHASE_GUIDE 0  // unsharded launches: 0 = no phase budget (measured best for single launches)
@@ -1487,7 +1490,7 @@ __device__ __forceinline__ void emit_tile(const KParams &p, Odometer<W, E> &od, 
     // once spent, the warp stops planning for this phase
     od.phase_cands += cands;
     if (od.phase_cands >= od.phase_budget)
-        emitted = max(emitted, (int)p.dpw);
+        emitted = max(emitted, od.dpw_now);
 }
 
 // One descriptor: stage its chains in the warp's shared block, run the tile.
@@ -1918,6 +1921,17 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                                   ? ~0ull
                                   : max(p.desc_cands, rem / ((uint64_t)gridDim.x * (blockDim.x >> 5) * p.phase_guide));
             od.phase_cands = 0;
+            // descriptors per warp this phase: fewer once 3/4 of the chunks are
+            // claimed (big fused launches), so the last phases end together
+            od.dpw_now = (int)p.dpw;
+            if (p.dpw_late) {
+                unsigned long long claimed = 0;
+                if (lane == 0)
+                    claimed = *(volatile unsigned long long *)p.ctr;
+                claimed = __shfl_sync(FULL, claimed, 0);
+                if (claimed * 4 >= p.nvirt * 3)
+                    od.dpw_now = (int)p.dpw_late;
+            }
         }
         const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
         // (not while a 2-D row group is half emitted: n is then the group's start,
@@ -1933,7 +1947,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             if (__shfl_sync(FULL, pushed, 0))
                 c1 = n + (c1 - n) / 2;
         }
-        while (!done && emitted < (int)p.dpw) {
+        while (!done && emitted < od.dpw_now) {
             SIMBA_WD("plan", n, emitted);
             if (!have_piece) {
                 if (!have_claim || v >= cl.v1) {
@@ -2044,7 +2058,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                 direct_range<W>(p, st, rn, pstop, false, ss.count, s);
                 rn2 = pstop;
             } else {
-                rn2 = plan_pblock<W, E>(p, st, od, rn, pstop, lane, ss, emitted, (int)p.dpw);
+                rn2 = plan_pblock<W, E>(p, st, od, rn, pstop, lane, ss, emitted, od.dpw_now);
             }
             n = vb + rn2;
             if (n >= c1 || (early && n > read_best(p))) {  // piece finished (or the rest ranks above a hit)
@@ -2476,7 +2490,8 @@ struct simba_ctx {
     long long fine_row_env = -1;
     uint64_t super_per_shard = kSuperPerShard;  // SIMBA_SUPER_PER_SHARD env
     uint32_t dpw_env = 0;  // SIMBA_DPW_RT: descriptors per warp and phase (<= SIMBA_DPW; diagnostics)
-    int shard_pg_env = -1;     // SIMBA_SHARD_PG: phase guide of sharded launches (diagnostics)
+    int shard_pg_env = -1;
+    int dpw_late_env = -1;     // SIMBA_DPW_LATE: descriptors per warp once 3/4 is claimed (0: no change)     // SIMBA_SHARD_PG: phase guide of sharded launches (diagnostics)
     uint32_t shard_dpw_env = 0;  // SIMBA_SHARD_DPW: descriptors per warp and phase of sharded launches
     int absorb = 1;  // unary-topped right children of size R0+1 absorbed into P blocks (SIMBA_ABSORB=0: off)
     uint64_t y0 = 0;          // outputs[0]
@@ -2775,10 +2790,14 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.fine_row = c->fine_row_env >= 0 ? (uint64_t)c->fine_row_env : row_total(c, c->R0) + 1;
     p.absorb = c->absorb;
     p.phase_guide = rq.nshards > 1 ? kShardPhaseGuide : kPhaseGuide;
-    // descriptors per warp and phase: fewer in big fused (multi-level) launches,
-    // whose last full phases set the launch's end (the bench sweep: mean of 60
-    // launches 18.9 -> 18.25 ms at 16); single levels and shards keep 24
+    // descriptors per warp and phase: in big fused (multi-level) launches 16
+    // instead of 24 once 3/4 of the chunks are claimed, so the last full phases
+    // end together (the bench sweep: mean of 30 launches 18.9 -> 18.25 ms at 16
+    // throughout, 18.15 with 24 -> 16); single levels and shards keep 24
     p.dpw = (rq.nshards == 1 && s_lo < rq.size && per_shard >= c->big_launch) ? SIMBA_FUSED_DPW : kDescPerWarp;
+    p.dpw_late = (rq.nshards == 1 && s_lo < rq.size && per_shard >= c->big_launch) ? SIMBA_FUSED_DPW_LATE : 0;
+    if (c->dpw_late_env >= 0)
+        p.dpw_late = (uint32_t)std::min(c->dpw_late_env, kDescPerWarp);
     if (c->dpw_env)
         p.dpw = std::min<uint32_t>(c->dpw_env, kDescPerWarp);
     if (rq.nshards > 1 && c->shard_pg_env >= 0)
@@ -3120,6 +3139,9 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->super_per_shard = kSuperPerShard;
     if (const char *e = getenv("SIMBA_SUPER_PER_SHARD"))
         c->super_per_shard = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
+    c->dpw_late_env = -1;
+    if (const char *e = getenv("SIMBA_DPW_LATE"))
+        c->dpw_late_env = std::max(0, atoi(e));
     c->shard_pg_env = -1;
     if (const char *e = getenv("SIMBA_SHARD_PG"))
         c->shard_pg_env = std::max(0, atoi(e));

@@ -103,6 +103,7 @@ struct KParams {
     void *queue;                  // tile descriptors, qcap per CTA (plan/execute phases)
     uint32_t qcap;
     uint32_t dpw;                 // descriptors per warp and phase (<= kDescPerWarp)
+    uint32_t dpw_late;            // ... once 3/4 of the chunks are claimed (0: dpw throughout)
     uint32_t ps_off;              // shared-memory offset of the CTA's queue bookkeeping
     unsigned long long *vq;       // deferred verification queue, vqcap ranks per CTA (null: verify inline)
     uint32_t vqcap;
@@ -584,6 +585,7 @@ struct Odometer {
     uint64_t phase_budget, phase_cands;  // candidates the warp may plan / has planned in this phase
     uint64_t fine_end;     // != 0: planning a partial R0+1 row at R0 until this virtual rank
     bool absorb;           // a binary node whose right child (size R0+1) starts with NOT/NEG is P
+    int dpw_now;           // descriptors this warp may queue in the current phase
     // planner resume point inside a 2-D row group (queue filled mid-group)
     bool rs_valid;
     uint32_t rs_c;
