@@ -1405,7 +1405,7 @@ constexpr int kBuckets = kVariants * kSizeClasses;
 
 struct PlanShared {
     unsigned int vqn;  // deferred verifications queued this phase (must stay the first field)
-    unsigned int qn, qnext, active;
+    unsigned int qn[2], qnext, active;  // queue sizes of the two buffers, execute counter, warps with work
     unsigned int start[kBuckets];
     uint8_t var[SIMBA_UNIT_THREADS / 32 * kDescPerWarp];
     uint16_t order[SIMBA_UNIT_THREADS / 32 * kDescPerWarp];
@@ -1418,9 +1418,9 @@ __device__ __forceinline__ PlanShared *plan_shared(const KParams &p)
 }
 
 template <class W, int E>
-__device__ __forceinline__ TileDesc<W, E> *desc_queue(const KParams &p)
+__device__ __forceinline__ TileDesc<W, E> *desc_queue(const KParams &p, unsigned int buf)
 {
-    return reinterpret_cast<TileDesc<W, E> *>(p.queue) + (size_t)blockIdx.x * p.qcap;
+    return reinterpret_cast<TileDesc<W, E> *>(p.queue) + ((size_t)blockIdx.x * 2 + buf) * p.qcap;
 }
 
 __device__ __forceinline__ int variant_of(int kind, int nt, uint64_t nrows)
@@ -1440,9 +1440,9 @@ __device__ __forceinline__ void emit_tile(const KParams &p, Odometer<W, E> &od, 
     const uint64_t cands = nrows * (uint64_t)(chi - clo);  // warp-uniform
     unsigned int slot = 0;
     if (lane == 0)
-        slot = atomicAdd(&ps->qn, 1u);
+        slot = atomicAdd(&ps->qn[od.qbuf], 1u);
     slot = __shfl_sync(FULL, slot, 0);
-    TileDesc<W, E> *d = desc_queue<W, E>(p) + slot;
+    TileDesc<W, E> *d = desc_queue<W, E>(p, od.qbuf) + slot;
     if (lane == 0) {
         d->ta = od.L->tac;
 #pragma unroll
@@ -1878,7 +1878,8 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
 #endif
     if (threadIdx.x == 0) {
         ps->vqn = 0;
-        ps->qn = 0;
+        ps->qn[0] = 0;
+        ps->qn[1] = 0;
         ps->qnext = 0;
         ps->active = 0;
     }
@@ -1896,12 +1897,39 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
         cta_dry = ~0ull;
     __syncthreads();
 #endif
+    // Pipelined phases: the queue has two buffers.  In each phase every warp
+    // executes tiles of the buffer sorted at the end of the previous phase
+    // until none is left, then plans the next phase into the other buffer.
+    unsigned int cur = 0, nq = 0;  // buffer being executed and its size (none in the first phase)
     for (;;) {
 #ifdef SIMBA_CTA_TIMES
         ++nphase;
         tp0 = globaltimer_ns();
 #endif
-        // ---- plan: advance the odometer, queue up to kDescPerWarp tiles
+        // ---- execute the queue sorted at the end of the previous phase
+        if (nq) {
+            const TileDesc<W, E> *q = desc_queue<W, E>(p, cur);
+            SIMBA_CYC_BEGIN(cwe);
+            for (;;) {
+                unsigned int idx = 0;
+                if (lane == 0)
+                    idx = atomicAdd(&ps->qnext, 1u);
+                idx = __shfl_sync(FULL, idx, 0);
+                if (idx >= nq)
+                    break;
+                SIMBA_WD("exec", idx, nq);
+                exec_desc<W, E>(p, st, q + ps->order[idx], lane, ss.count);
+            }
+            SIMBA_CYC_END(p, ST_W_EXEC, cwe);
+            if (lane == 0)
+                od.L->tac_gen = ~0u;  // the tiles reused the warp's block: refold next time
+            __syncwarp();
+        }
+        // ---- plan the next phase into the other buffer: a warp starts as soon
+        // as the executing queue has nothing left for it, while other warps
+        // still run their last tiles (the phase's execute tail and the planning
+        // overlap instead of following each other across a barrier)
+        od.qbuf = cur ^ 1u;
         SIMBA_WD("phase", n, c1);
         if (threadIdx.x == 0)
             pull_xbest(p);  // the other shards' hits (read_best below sees them)
@@ -2072,29 +2100,44 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
         if (lane == 0 && !done)
             atomicAdd(&ps->active, 1u);
         __syncthreads();
-#ifdef SIMBA_STATS
-        if (threadIdx.x == 0) {
-            atomicAdd(&p.stats[2 * ST_PH_PLAN], 1ull);
-            atomicAdd(&p.stats[2 * ST_PH_PLAN + 1], (unsigned long long)(clock64() - cph));
-        }
-        const long long cpe = clock64();
-#endif
-        const unsigned int nq = ps->qn;
-        if (nq == 0 && ps->active == 0)
-            break;  // uniform: every warp is done and nothing is queued
 #ifdef SIMBA_CTA_TIMES
-        tx0 = globaltimer_ns();
-        if (tx0 - tp0 > mp_ns) {
-            mp_ns = tx0 - tp0;
-            mp_at = tp0;
+        {
+            const unsigned long long tx1 = globaltimer_ns();
+            if (tx1 - tp0 > mx_ns) {
+                mx_ns = tx1 - tp0;
+                mx_at = tp0;
+                mx_q = nq;
+            }
         }
 #endif
-        // ---- sort the queue by tile variant (counting sort, warp 0)
+        // ---- verify the deferred candidates of this phase's tiles with every thread
+        {
+            const unsigned int nv = min(ps->vqn, p.vqcap);
+            const unsigned long long *vq = p.vq + (size_t)blockIdx.x * p.vqcap;
+            for (unsigned int i = threadIdx.x; i < nv; i += blockDim.x) {
+                const int ls = level_of(p, vq[i]);
+                const uint64_t r = vq[i] - p.vbase[ls];
+                if (full_check<W>(p, st, r, ls))
+                    record_hit(p, ls, r, ss.count);
+            }
+        }
+        const unsigned int nn = ps->qn[cur ^ 1u];
+        const bool finish = nn == 0 && ps->active == 0;  // uniform: no work queued or left
+        __syncthreads();
+        if (finish)
+            break;
+        if (threadIdx.x == 0) {
+            ps->vqn = 0;
+            ps->qn[cur] = 0;
+            ps->qnext = 0;
+            ps->active = 0;
+        }
+        // ---- sort the next queue by size class and tile variant (counting sort, warp 0)
         if (threadIdx.x < 32) {
             for (int k = lane; k < kBuckets; k += 32)
                 ps->start[k] = 0;
             __syncwarp();
-            for (unsigned int i = lane; i < nq; i += 32)
+            for (unsigned int i = lane; i < nn; i += 32)
                 atomicAdd(&ps->start[ps->var[i]], 1u);
             __syncwarp();
             if (lane == 0) {
@@ -2106,70 +2149,12 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                 }
             }
             __syncwarp();
-            for (unsigned int i = lane; i < nq; i += 32)
+            for (unsigned int i = lane; i < nn; i += 32)
                 ps->order[atomicAdd(&ps->start[ps->var[i]], 1u)] = (uint16_t)i;
         }
         __syncthreads();
-        // ---- execute: all warps drain the queue variant by variant
-        const TileDesc<W, E> *q = desc_queue<W, E>(p);
-        SIMBA_CYC_BEGIN(cwe);
-        for (;;) {
-            unsigned int idx = 0;
-            if (lane == 0)
-                idx = atomicAdd(&ps->qnext, 1u);
-            idx = __shfl_sync(FULL, idx, 0);
-            if (idx >= nq)
-                break;
-            SIMBA_WD("exec", idx, nq);
-            exec_desc<W, E>(p, st, q + ps->order[idx], lane, ss.count);
-        }
-        SIMBA_CYC_END(p, ST_W_EXEC, cwe);
-        __syncthreads();
-#ifdef SIMBA_CTA_TIMES
-        {
-            const unsigned long long tx1 = globaltimer_ns();
-            if (tx1 - tx0 > mx_ns) {
-                mx_ns = tx1 - tx0;
-                mx_at = tx0;
-                mx_q = nq;
-            }
-        }
-#endif
-#ifdef SIMBA_STATS
-        if (threadIdx.x == 0) {
-            atomicAdd(&p.stats[2 * ST_PH_EXEC], 1ull);
-            atomicAdd(&p.stats[2 * ST_PH_EXEC + 1], (unsigned long long)(clock64() - cpe));
-        }
-        const long long cpv = clock64();
-#endif
-        // ---- verify the deferred candidates with every thread of the CTA
-        {
-            const unsigned int nv = min(ps->vqn, p.vqcap);
-            const unsigned long long *vq = p.vq + (size_t)blockIdx.x * p.vqcap;
-            for (unsigned int i = threadIdx.x; i < nv; i += blockDim.x) {
-                const int ls = level_of(p, vq[i]);
-                const uint64_t r = vq[i] - p.vbase[ls];
-                if (full_check<W>(p, st, r, ls))
-                    record_hit(p, ls, r, ss.count);
-            }
-        }
-        __syncthreads();
-#ifdef SIMBA_STATS
-        if (threadIdx.x == 0) {
-            atomicAdd(&p.stats[2 * ST_PH_VERIFY], (unsigned long long)nq);
-            atomicAdd(&p.stats[2 * ST_PH_VERIFY + 1], (unsigned long long)(clock64() - cpv));
-        }
-#endif
-        if (threadIdx.x == 0)
-            ps->vqn = 0;
-        if (threadIdx.x == 0) {
-            ps->qn = 0;
-            ps->qnext = 0;
-            ps->active = 0;
-        }
-        if (lane == 0)
-            od.L->tac_gen = ~0u;  // the tiles reused the warp's block: refold next time
-        __syncthreads();
+        cur ^= 1u;
+        nq = nn;
     }
     flush_counts(p, ss.count, vis, ss.units, ss.rank_units);
 #ifdef SIMBA_CTA_TIMES
@@ -3232,7 +3217,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         const size_t o_tok = up(o_ctr + sizeof(unsigned long long) * kCtrWords);
         const size_t o_stats = up(o_tok + sizeof(int32_t) * MAXS);
         const size_t o_queue = up(o_stats + sizeof(unsigned long long) * 2 * ST_N);
-        const size_t o_vq = up(o_queue + db * c->qcap * (size_t)sms * 2);  // two CTAs per SM at most
+        const size_t o_vq = up(o_queue + db * c->qcap * (size_t)sms * 2 * 2);  // two CTAs per SM at most, two buffers
         const size_t o_lvl = up(o_vq + sizeof(unsigned long long) * kVerifyCap * (size_t)sms * 2);
         const size_t o_pool = up(o_lvl + sizeof(unsigned long long) * (kLvlWords + MAXS + 2));
         const size_t total = up(o_pool + sizeof(unsigned long long) * (1 + 3 * kPoolSlots));

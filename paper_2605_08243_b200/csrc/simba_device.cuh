@@ -586,6 +586,7 @@ struct Odometer {
     uint64_t fine_end;     // != 0: planning a partial R0+1 row at R0 until this virtual rank
     bool absorb;           // a binary node whose right child (size R0+1) starts with NOT/NEG is P
     int dpw_now;           // descriptors this warp may queue in the current phase
+    unsigned int qbuf;     // the queue buffer this warp plans into
     // planner resume point inside a 2-D row group (queue filled mid-group)
     bool rs_valid;
     uint32_t rs_c;

@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests/test_production_paths.py -q -x 2>&1 | tail -1
+for i in 1 2; do for cfg in "X=1" "SIMBA_DPW_LATE=16" "SIMBA_DPW_LATE=12"; do
+  echo "== $cfg"; env $cfg timeout 300 python scripts/probe_shapes.py 0:0; env $cfg timeout 300 python scripts/probe_shards.py 8
+done; done
