@@ -1368,7 +1368,7 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 #endif
 constexpr int kDescPerWarp = SIMBA_DPW;
 #ifndef SIMBA_FUSED_DPW_LATE
-#define SIMBA_FUSED_DPW_LATE 16  // big fused launches once 3/4 of the chunks are claimed
+#define SIMBA_FUSED_DPW_LATE 12  // big fused launches once 3/4 of the chunks are claimed
 #endif
 #ifndef SIMBA_FUSED_DPW
 #define SIMBA_FUSED_DPW 24
