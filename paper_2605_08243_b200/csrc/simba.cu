@@ -1367,6 +1367,9 @@ __device__ __forceinline__ void dispatch_cf(const KParams &p, const Staged &st, 
 #define SIMBA_DESC_LOG2 18
 #endif
 constexpr int kDescPerWarp = SIMBA_DPW;
+#ifndef SIMBA_FUSED_DESC_SHIFT
+#define SIMBA_FUSED_DESC_SHIFT 1
+#endif
 #ifndef SIMBA_FUSED_DPW_LATE
 #define SIMBA_FUSED_DPW_LATE 12  // big fused launches once 3/4 of the chunks are claimed
 #endif
@@ -2743,6 +2746,11 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     // use R0 + 1; large launches use larger descriptors and claims
     const uint64_t per_shard = range / rq.nshards;
     p.desc_cands = per_shard >= c->big_launch ? kDescCandsBig : kDescCandsBig / 2;
+    // big fused (multi-level) launches: twice that (with the pipelined phases
+    // the longer descriptors cost no tail there: sweep mean 17.65 -> 17.3 ms; a
+    // single size-13 launch is 10% slower with them, so it keeps 2^18)
+    if (rq.nshards == 1 && s_lo < rq.size && per_shard >= c->big_launch)
+        p.desc_cands = kDescCandsBig << SIMBA_FUSED_DESC_SHIFT;
     p.guide = per_shard >= c->big_launch ? (s_lo < rq.size ? SIMBA_FUSED_GUIDE : kGuideBig) : 2 * kGuideBig;
 #if SIMBA_SHARD_GUIDE
     if (rq.nshards > 1)

@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests/test_production_paths.py -q -x 2>&1 | tail -1
+for i in 1 2; do for lib in libsimba.so libsimba_fd0.so libsimba_fd2.so; do
+  echo "== $lib"; SIMBA_LIB=$PWD/paper_2605_08243_b200/_lib/$lib timeout 300 python scripts/probe_variance.py 30; SIMBA_LIB=$PWD/paper_2605_08243_b200/_lib/$lib timeout 300 python scripts/probe_shapes.py 0:0
+done; done
