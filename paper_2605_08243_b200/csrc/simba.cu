@@ -1530,6 +1530,29 @@ __device__ __noinline__ void exec_desc(const KParams &p, const Staged &st, const
         __trap();
     }
 #endif
+#ifdef SIMBA_STATS
+    if (d->nt > 0) {
+        const uint64_t cands = d->kind == 0 ? d->nrows * (uint64_t)(d->chi - d->clo) : d->nrows * (uint64_t)d->R2;
+        SIMBA_STAT(p, d->nt == 1 ? ST_GEN_NT1 : d->nt == 2 ? ST_GEN_NT2 : ST_GEN_NT3, cands);
+        if (d->pop == OP_ADD || d->pop == OP_SUB || d->pop == OP_MUL)
+            SIMBA_STAT(p, ST_GEN_ARITH, cands);
+        const int k0 = gen_merges(d->pop, d->ta) ? 1 : 0;
+        bool aff = true, bw = true;
+        for (int i = k0; i < d->ta.nres; ++i) {
+            const Seg<W> &g = d->ta.res[i];
+            if (!(g.m == (W)~(W)0 && g.x == (W)0))
+                aff = false;
+            if (!(g.a == (W)1 && g.b == (W)0))
+                bw = false;
+        }
+        if (d->ta.nres > k0) {
+            if (aff)
+                SIMBA_STAT(p, ST_GEN_RES_AFF, cands);
+            if (bw)
+                SIMBA_STAT(p, ST_GEN_RES_BW, cands);
+        }
+    }
+#endif
     const XU xu{d->x2d, d->pxop, d->szy, d->sz1, d->offy, d->off1, d->R1p};
     if (d->kind == 0)
         dispatch_rf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, d->clo, d->chi,

@@ -25,6 +25,9 @@ enum : int {
     ST_PH_PLAN, ST_PH_EXEC, ST_PH_VERIFY,  // (phases, CTA cycles) of each phase (thread 0)
     ST_W_PLAN, ST_W_EXEC,                 // (warp phases, warp busy cycles) inside plan / exec
     ST_ROW_NONE,                          // one-row tiles of a P-less region (a unary node above L2)
+    ST_GEN_NT1, ST_GEN_NT2, ST_GEN_NT3,   // GEN candidates by segments per candidate (3: 3 or more)
+    ST_GEN_ARITH,                         // GEN candidates of an arithmetic P
+    ST_GEN_RES_AFF, ST_GEN_RES_BW,        // GEN candidates whose residual segments are all affine / all bitwise
     ST_N
 };
 #ifdef SIMBA_STATS

@@ -266,7 +266,8 @@ class DeviceContext:
         return h.value or 0
 
     PATHS = ("rf_fold", "rf_gen", "rf_row", "cf_fold", "cf_gen", "cyc_outer", "cyc_x", "cyc_tile", "direct",
-             "ph_plan", "ph_exec", "ph_verify", "w_plan", "w_exec", "row_none")
+             "ph_plan", "ph_exec", "ph_verify", "w_plan", "w_exec", "row_none", "gen_nt1", "gen_nt2", "gen_nt3",
+             "gen_arith", "gen_res_aff", "gen_res_bw")
 
     def path_stats(self) -> dict:
         """Per-path (calls, candidates) of the unit kernel since creation;
