@@ -2504,6 +2504,7 @@ struct simba_ctx {
     int shard_pg_env = -1;
     int dpw_late_env = -1;     // SIMBA_DPW_LATE: descriptors per warp once 3/4 is claimed (0: no change)     // SIMBA_SHARD_PG: phase guide of sharded launches (diagnostics)
     uint32_t shard_dpw_env = 0;  // SIMBA_SHARD_DPW: descriptors per warp and phase of sharded launches
+    int fused_shards = 1;  // big shards take the one-GPU sweep's launch shape (SIMBA_FUSED_SHARDS=0: not)
     int absorb = 1;  // unary-topped right children of size R0+1 absorbed into P blocks (SIMBA_ABSORB=0: off)
     uint64_t y0 = 0;          // outputs[0]
     bool value_tables_by_decode = false;  // SIMBA_VT_DECODE=1: per-entry decode + eval (the cross-check)
@@ -2772,11 +2773,15 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     // big fused (multi-level) launches: twice that (with the pipelined phases
     // the longer descriptors cost no tail there: sweep mean 17.65 -> 17.3 ms; a
     // single size-13 launch is 10% slower with them, so it keeps 2^18)
-    if (rq.nshards == 1 && s_lo < rq.size && per_shard >= c->big_launch)
+    // (big shards of a multi-GPU job, >= big_launch candidates each, are shaped
+    // like the one-GPU sweep when fused_shards is set)
+    const bool fused_big = s_lo < rq.size && per_shard >= c->big_launch && (rq.nshards == 1 || c->fused_shards);
+    const bool shard_rules = rq.nshards > 1 && !fused_big;
+    if (fused_big)
         p.desc_cands = kDescCandsBig << SIMBA_FUSED_DESC_SHIFT;
     p.guide = per_shard >= c->big_launch ? (s_lo < rq.size ? SIMBA_FUSED_GUIDE : kGuideBig) : 2 * kGuideBig;
 #if SIMBA_SHARD_GUIDE
-    if (rq.nshards > 1)
+    if (shard_rules)
         p.guide = SIMBA_SHARD_GUIDE;
 #endif
     // R0 + 1 needs long claims: rows of T[R0+1] columns cut at every claim
@@ -2805,13 +2810,13 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     // partial rows of size-(R0+1) super-leaves are planned at R0 (rows of T[R0])
     p.fine_row = c->fine_row_env >= 0 ? (uint64_t)c->fine_row_env : row_total(c, c->R0) + 1;
     p.absorb = c->absorb;
-    p.phase_guide = rq.nshards > 1 ? kShardPhaseGuide : kPhaseGuide;
+    p.phase_guide = shard_rules ? kShardPhaseGuide : kPhaseGuide;
     // descriptors per warp and phase: in big fused (multi-level) launches 16
     // instead of 24 once 3/4 of the chunks are claimed, so the last full phases
     // end together (the bench sweep: mean of 30 launches 18.9 -> 18.25 ms at 16
     // throughout, 18.15 with 24 -> 16); single levels and shards keep 24
-    p.dpw = (rq.nshards == 1 && s_lo < rq.size && per_shard >= c->big_launch) ? SIMBA_FUSED_DPW : kDescPerWarp;
-    p.dpw_late = (rq.nshards == 1 && s_lo < rq.size && per_shard >= c->big_launch) ? SIMBA_FUSED_DPW_LATE : 0;
+    p.dpw = fused_big ? SIMBA_FUSED_DPW : kDescPerWarp;
+    p.dpw_late = fused_big ? SIMBA_FUSED_DPW_LATE : 0;
     if (c->dpw_late_env >= 0)
         p.dpw_late = (uint32_t)std::min(c->dpw_late_env, kDescPerWarp);
     if (c->dpw_env)
@@ -3167,6 +3172,9 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->dpw_env = 0;
     if (const char *e = getenv("SIMBA_DPW_RT"))
         c->dpw_env = (uint32_t)std::max(1, atoi(e));
+    c->fused_shards = 1;  // 2-way shards of the C5 sweep: 11.3 -> 9.8 ms
+    if (const char *e = getenv("SIMBA_FUSED_SHARDS"))
+        c->fused_shards = atoi(e) != 0;
     c->absorb = 1;
     if (const char *e = getenv("SIMBA_ABSORB"))
         c->absorb = atoi(e) != 0;
