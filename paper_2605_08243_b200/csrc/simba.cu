@@ -1492,8 +1492,10 @@ __device__ __forceinline__ void emit_tile(const KParams &p, Odometer<W, E> &od, 
     // the phase's candidate budget (shrinks with the launch's remaining work):
     // once spent, the warp stops planning for this phase
     od.phase_cands += cands;
-    if (od.phase_cands >= od.phase_budget)
+    if (od.phase_cands >= od.phase_budget) {
         emitted = max(emitted, od.dpw_now);
+        od.emit_max = 0;  // (shared-cap mode) this warp's planning ends with the phase budget
+    }
 }
 
 // One descriptor: stage its chains in the warp's shared block, run the tile.
@@ -1560,6 +1562,27 @@ __device__ __noinline__ void exec_desc(const KParams &p, const Staged &st, const
     else
         dispatch_cf<W, E>(p, st, d->pop, d->nt, xu, d->ubase, d->R2, d->off2, d->row0, d->nrows, lane, cnt);
     __syncwarp();
+}
+
+// Whether this warp stops planning for the phase: its own descriptor limit,
+// or (shared_cap) the CTA's queue is as full as the phase allows -- warps then
+// keep planning until the queue fills instead of each stopping at an equal
+// share, so they all reach the phase barrier at about the same time (a warp
+// whose units are costly to plan no longer holds the other fifteen there).
+template <class W, int E>
+__device__ __forceinline__ bool plan_stop(const KParams &p, const Odometer<W, E> &od, int emitted, int cap, int lane)
+{
+    if (!p.shared_cap)
+        return emitted >= cap;
+    if (emitted >= od.emit_max)  // the phase budget (sharded launches) ended this warp's planning
+        return true;
+    unsigned int q = 0;
+    if (lane == 0)
+        q = *(volatile unsigned int *)&plan_shared(p)->qn[od.qbuf];
+    q = __shfl_sync(FULL, q, 0);
+    const unsigned int warps = blockDim.x >> 5;
+    // (at most one emit per warp can follow a check: the margin keeps slot < qcap)
+    return q + warps >= min(p.qcap, (uint32_t)cap * warps);
 }
 
 // All ranks [n, n1) of one P block (n1 <= pend).  The outer chain and P's
@@ -1652,7 +1675,7 @@ __device__ __forceinline__ uint64_t plan_pblock(const KParams &p, const Staged &
             const uint64_t dc = p.desc_cands;
             const uint64_t rmax = max((uint64_t)1, dc / R2);
             while (u < u1) {
-                if (emitted >= cap)
+                if (plan_stop(p, od, emitted, cap, lane))
                     return ubase + u;  // queue full: resume here in the next phase
                 const uint64_t d1 = (pop == OP_NONE) ? 0 : div_T(t, prsz, u);
                 const uint64_t rs = d1 * R2;
@@ -1673,7 +1696,7 @@ __device__ __forceinline__ uint64_t plan_pblock(const KParams &p, const Staged &
                         cc = od.rs_c;
                     od.rs_valid = false;
                     for (; cc < R2; cc += cw) {
-                        if (emitted >= cap) {
+                        if (plan_stop(p, od, emitted, cap, lane)) {
                             od.rs_valid = true;
                             od.rs_n = ubase + u;
                             od.rs_c = cc;
@@ -1975,6 +1998,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                                   ? ~0ull
                                   : max(p.desc_cands, rem / ((uint64_t)gridDim.x * (blockDim.x >> 5) * p.phase_guide));
             od.phase_cands = 0;
+            od.emit_max = 1 << 30;
             // descriptors per warp this phase: fewer once 3/4 of the chunks are
             // claimed (big fused launches), so the last phases end together
             od.dpw_now = (int)p.dpw;
@@ -2001,7 +2025,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
             if (__shfl_sync(FULL, pushed, 0))
                 c1 = n + (c1 - n) / 2;
         }
-        while (!done && emitted < od.dpw_now) {
+        while (!done && !plan_stop(p, od, emitted, od.dpw_now, lane)) {
             SIMBA_WD("plan", n, emitted);
             if (!have_piece) {
                 if (!have_claim || v >= cl.v1) {
@@ -2504,6 +2528,7 @@ struct simba_ctx {
     int shard_pg_env = -1;
     int dpw_late_env = -1;     // SIMBA_DPW_LATE: descriptors per warp once 3/4 is claimed (0: no change)     // SIMBA_SHARD_PG: phase guide of sharded launches (diagnostics)
     uint32_t shard_dpw_env = 0;  // SIMBA_SHARD_DPW: descriptors per warp and phase of sharded launches
+    int shared_cap = 1;    // warps plan until the CTA queue fills (SIMBA_SHARED_CAP=0: equal shares)
     int fused_shards = 1;  // big shards take the one-GPU sweep's launch shape (SIMBA_FUSED_SHARDS=0: not)
     int absorb = 1;  // unary-topped right children of size R0+1 absorbed into P blocks (SIMBA_ABSORB=0: off)
     uint64_t y0 = 0;          // outputs[0]
@@ -2810,6 +2835,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     // partial rows of size-(R0+1) super-leaves are planned at R0 (rows of T[R0])
     p.fine_row = c->fine_row_env >= 0 ? (uint64_t)c->fine_row_env : row_total(c, c->R0) + 1;
     p.absorb = c->absorb;
+    p.shared_cap = c->shared_cap && !shard_rules;  // (small shards: 3.67 vs 3.75 ms with equal shares)
     p.phase_guide = shard_rules ? kShardPhaseGuide : kPhaseGuide;
     // descriptors per warp and phase: in big fused (multi-level) launches 16
     // instead of 24 once 3/4 of the chunks are claimed, so the last full phases
@@ -3172,6 +3198,9 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->dpw_env = 0;
     if (const char *e = getenv("SIMBA_DPW_RT"))
         c->dpw_env = (uint32_t)std::max(1, atoi(e));
+    c->shared_cap = 1;
+    if (const char *e = getenv("SIMBA_SHARED_CAP"))
+        c->shared_cap = atoi(e) != 0;
     c->fused_shards = 1;  // 2-way shards of the C5 sweep: 11.3 -> 9.8 ms
     if (const char *e = getenv("SIMBA_FUSED_SHARDS"))
         c->fused_shards = atoi(e) != 0;

@@ -115,6 +115,7 @@ struct KParams {
     int s_lo, s_hi;
     uint64_t fine_row;  // partial rows of at least this many columns at R0 + 1 levels are planned at R0 (0: off)
     int absorb;         // Odometer::absorb (SIMBA_ABSORB)
+    int shared_cap;     // planning stops when the CTA queue is full (else at an equal share per warp)
     const unsigned long long *vbase;  // [MAXS + 2] (global; kept out of the parameter block)
     unsigned long long *lvl;      // per level: [s] count, [MAXS+1+s] visited, [2*(MAXS+1)+s] first rank
 };
@@ -590,6 +591,7 @@ struct Odometer {
     bool absorb;           // a binary node whose right child (size R0+1) starts with NOT/NEG is P
     int dpw_now;           // descriptors this warp may queue in the current phase
     unsigned int qbuf;     // the queue buffer this warp plans into
+    int emit_max;          // 0 once the phase budget ended this warp's planning (shared-cap mode)
     // planner resume point inside a 2-D row group (queue filled mid-group)
     bool rs_valid;
     uint32_t rs_c;
