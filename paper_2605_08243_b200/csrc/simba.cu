@@ -1745,7 +1745,7 @@ struct Claim {
 // they finish.  A pusher always returns to the pool before exiting, so every
 // pushed range is taken.  Slot state: 0 empty, 1 full, 2/3 being written/read.
 #ifndef SIMBA_SPLIT_MIN_LOG2
-#define SIMBA_SPLIT_MIN_LOG2 17  // 2^19: sweep mean 19.1-19.4 ms over 40 launches, 2^17: 18.6-18.9
+#define SIMBA_SPLIT_MIN_LOG2 19  // 2^17 was better before the pipelined phases and the shared queue cap (18.6-18.9 vs 19.1-19.4 ms), 2^19 after (16.4-16.65 vs 16.7-16.8)
 #endif
 constexpr uint64_t kSplitMin = SIMBA_SPLIT_MIN_LOG2 ? 1ull << SIMBA_SPLIT_MIN_LOG2 : 0;  // 0: no splitting
 
