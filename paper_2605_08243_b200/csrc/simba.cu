@@ -2273,13 +2273,14 @@ __global__ void ex0_density_kernel(const W *g, uint32_t len, W y0, W mask, unsig
 // of eval_tokens, in the same full word width (so the values equal
 // value_table_kernel's decode + eval_rpn per entry, at a fraction of the work).
 template <class W>
-__global__ void value_level_kernel(const Tabs *tabs, const W *X, int k, int sz, int E, uint32_t tbl_len, W *out)
+__global__ void value_level_kernel(const Tabs *tabs, const W *X, int k, int sz, int e0, int E, uint32_t tbl_len,
+                                   W *out)
 {
     const uint32_t n = (uint32_t)tabs->T[sz];
     const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (uint32_t)E * n)
+    if (idx >= (uint32_t)(E - e0) * n)
         return;
-    const uint32_t e = idx / n, r = idx - e * n;
+    const uint32_t e = e0 + idx / n, r = idx % n;
     W *g = out + (size_t)e * tbl_len;
     W v;
     if (sz == 1) {
@@ -2303,19 +2304,20 @@ __global__ void value_level_kernel(const Tabs *tabs, const W *X, int k, int sz, 
 }
 
 template <class W>
-__global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int RG, int E, uint32_t tbl_len, W *out)
+__global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int RG, int e0, int E, uint32_t tbl_len,
+                                   W *out)
 {
     const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (uint32_t)E * tbl_len)
+    if (idx >= (uint32_t)(E - e0) * tbl_len)
         return;
-    const uint32_t e = idx / tbl_len;
-    const uint32_t j = idx - e * tbl_len;
+    const uint32_t e = e0 + idx / tbl_len;
+    const uint32_t j = idx % tbl_len;
     int sz = 1;
     while (sz < RG && tabs->toff[sz + 1] <= j)
         ++sz;
     int8_t buf[MAXS];
     decode_tokens(tabs, j - tabs->toff[sz], sz, buf);
-    out[idx] = eval_rpn<W, W>(buf, sz, X + (size_t)e * k);
+    out[(size_t)e * tbl_len + j] = eval_rpn<W, W>(buf, sz, X + (size_t)e * k);
 }
 
 // INT32 issue roofline probe: 8 independent LOP3 -> IMAD chains per thread
@@ -2512,6 +2514,75 @@ void pool_put(int device, void *p, size_t bytes, bool host)
     g_pool.push_back(PoolBlock{device, host, bytes, p});
 }
 
+// Streams and their timing events, pooled like the arenas: creating and
+// destroying a stream per context cost 0.06 ms per synthesize call, and a
+// stream creation right after a destroy occasionally blocked for 5-15 ms.
+struct StreamSet {
+    int device;
+    cudaStream_t stream;
+    cudaEvent_t ev0, ev1;
+};
+std::vector<StreamSet> g_streams;
+
+cudaError_t stream_get(int device, StreamSet *out)
+{
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (size_t i = 0; i < g_streams.size(); ++i)
+            if (g_streams[i].device == device) {
+                *out = g_streams[i];
+                g_streams.erase(g_streams.begin() + i);
+                return cudaSuccess;
+            }
+    }
+    StreamSet s{device, nullptr, nullptr, nullptr};
+    cudaError_t e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess)
+        e = cudaEventCreate(&s.ev0);
+    if (e == cudaSuccess)
+        e = cudaEventCreate(&s.ev1);
+    if (e != cudaSuccess) {
+        if (s.ev0)
+            cudaEventDestroy(s.ev0);
+        if (s.stream)
+            cudaStreamDestroy(s.stream);
+        return e;
+    }
+    *out = s;
+    return cudaSuccess;
+}
+
+void stream_put(const StreamSet &s)  // the stream is idle
+{
+    cudaStreamAttrValue a{};  // no access-policy window carried into the next context
+    cudaStreamSetAttribute(s.stream, cudaStreamAttributeAccessPolicyWindow, &a);
+    cudaGetLastError();
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_streams.push_back(s);
+}
+
+// SIMBA_TRACE_CTX=1: host-side phase times of context creation on stderr
+// (diagnostics for time-to-solve, where creation is part of every call).
+struct CtxTrace {
+    bool on = false;
+    std::chrono::steady_clock::time_point t0;
+    CtxTrace()
+    {
+        const char *e = getenv("SIMBA_TRACE_CTX");
+        on = e && atoi(e) != 0;
+        t0 = std::chrono::steady_clock::now();
+    }
+    void operator()(const char *what, cudaStream_t s = nullptr)
+    {
+        if (!on)
+            return;
+        if (s)
+            cudaStreamSynchronize(s);
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        fprintf(stderr, "[simba ctx] %8.3f ms  %s\n", ms, what);
+    }
+};
+
 }  // namespace
 
 struct simba_ctx {
@@ -2522,18 +2593,17 @@ struct simba_ctx {
     uint32_t guide_env = 0;  // SIMBA_GUIDE override of the claim guide (diagnostics)
     uint64_t big_launch = 0;  // candidates per shard from which launches use the big shapes (SIMBA_BIG_LAUNCH)
     uint64_t r0_rows = SIMBA_R0_ROWS;  // R0 + 1 needs first claims of this many rows (SIMBA_R0_ROWS env)
-    long long fine_row_env = -1;
+    long long fine_row_env = -1;  // SIMBA_FINE_ROW override of KParams::fine_row (0: off; diagnostics)
     uint64_t super_per_shard = kSuperPerShard;  // SIMBA_SUPER_PER_SHARD env
     uint32_t dpw_env = 0;  // SIMBA_DPW_RT: descriptors per warp and phase (<= SIMBA_DPW; diagnostics)
-    int shard_pg_env = -1;
-    int dpw_late_env = -1;     // SIMBA_DPW_LATE: descriptors per warp once 3/4 is claimed (0: no change)     // SIMBA_SHARD_PG: phase guide of sharded launches (diagnostics)
+    int shard_pg_env = -1;     // SIMBA_SHARD_PG: phase guide of sharded launches (diagnostics)
+    int dpw_late_env = -1;     // SIMBA_DPW_LATE: descriptors per warp once 3/4 is claimed (0: no change)
     uint32_t shard_dpw_env = 0;  // SIMBA_SHARD_DPW: descriptors per warp and phase of sharded launches
     int shared_cap = 1;    // warps plan until the CTA queue fills (SIMBA_SHARED_CAP=0: equal shares)
     int fused_shards = 1;  // big shards take the one-GPU sweep's launch shape (SIMBA_FUSED_SHARDS=0: not)
     int absorb = 1;  // unary-topped right children of size R0+1 absorbed into P blocks (SIMBA_ABSORB=0: off)
-    uint64_t y0 = 0;          // outputs[0]
     bool value_tables_by_decode = false;  // SIMBA_VT_DECODE=1: per-entry decode + eval (the cross-check)
-    double ex0_dense = 1e-4;  // example-0 match share of the value table from which E = 4 (SIMBA_EX0_DENSE)  // SIMBA_FINE_ROW override of KParams::fine_row (0: off; diagnostics)
+    double ex0_dense = 1e-4;  // example-0 match share of the value table from which E = 4 (SIMBA_EX0_DENSE)
     uint64_t last_super = 0;  // ranks per round-robin super-chunk of the last request
     uint64_t split_min = 0;  // pieces with at least this many ranks left split once claims run dry
     uint32_t tbl_len = 0, gtbl_len = 0, tbl_bytes = 0, ex_bytes = 0;
@@ -2596,22 +2666,24 @@ int setup_kernels(simba_ctx *c)
     return SIMBA_OK;
 }
 
+// Value tables of examples e0..E-1 (0: all; 1: the per-example tables added
+// when example 0 proves dense, next to its own).
 template <class W>
-int build_value_tables(simba_ctx *c)
+int build_value_tables(simba_ctx *c, int e0)
 {
     const int bt = 256;
     const W *X = reinterpret_cast<const W *>(c->d_blob + c->tbl_bytes);
     W *G = reinterpret_cast<W *>(c->d_gtbl);
     if (c->value_tables_by_decode) {  // reference-exact decode + eval per entry (SIMBA_VT_DECODE=1; tests)
-        const uint32_t total = (uint32_t)c->E * c->gtbl_len;
-        value_table_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(c->d_tabs, X, c->k, c->RG, c->E,
+        const uint32_t total = (uint32_t)(c->E - e0) * c->gtbl_len;
+        value_table_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(c->d_tabs, X, c->k, c->RG, e0, c->E,
                                                                             c->gtbl_len, G);
         g_launches++;
         CK(cudaGetLastError());
     } else {  // bottom-up, one launch per size (each level reads only the ones below)
         for (int sz = 1; sz <= c->RG; ++sz) {
-            const uint32_t total = (uint32_t)c->E * (uint32_t)c->h_tabs.T[sz];
-            value_level_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(c->d_tabs, X, c->k, sz, c->E,
+            const uint32_t total = (uint32_t)(c->E - e0) * (uint32_t)c->h_tabs.T[sz];
+            value_level_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(c->d_tabs, X, c->k, sz, e0, c->E,
                                                                               c->gtbl_len, G);
             g_launches++;
             CK(cudaGetLastError());
@@ -2656,17 +2728,43 @@ void l2_persist(simba_ctx *c)
     cudaGetLastError();  // best effort
 }
 
+// matches[e] = entries of example e's value table equal to its output, e < E
+// (one launch per example, one read-back)
 template <class W>
-int ex0_density(simba_ctx *c, unsigned long long *matches, int e = 0, uint64_t y = 0)
+int densities(simba_ctx *c, int E, const uint64_t *outputs, unsigned long long *matches)
 {
-    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(unsigned long long), c->stream));
-    ex0_density_kernel<W><<<296, 256, 0, c->stream>>>(reinterpret_cast<const W *>(c->d_gtbl) + (size_t)e * c->gtbl_len,
-                                                      c->gtbl_len, (W)(e ? y : c->y0), (W)c->mask, c->d_ctr);
+    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(unsigned long long) * E, c->stream));
+    for (int e = 0; e < E; ++e) {
+        ex0_density_kernel<W><<<296, 256, 0, c->stream>>>(reinterpret_cast<const W *>(c->d_gtbl) + (size_t)e * c->gtbl_len,
+                                                          c->gtbl_len, (W)outputs[e], (W)c->mask, c->d_ctr + e);
+        g_launches++;
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(unsigned long long) * E, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int e = 0; e < E; ++e)
+        matches[e] = c->h_ctr[e];
+    return SIMBA_OK;
+}
+
+template <class W>
+__global__ void swap_slices_kernel(W *a, W *b, uint32_t len)
+{
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+        const W t = a[i];
+        a[i] = b[i];
+        b[i] = t;
+    }
+}
+
+// exchange the value-table slices of examples 0 and e
+template <class W>
+int swap_slices(simba_ctx *c, int e)
+{
+    W *g = reinterpret_cast<W *>(c->d_gtbl);
+    swap_slices_kernel<W><<<592, 256, 0, c->stream>>>(g, g + (size_t)e * c->gtbl_len, c->gtbl_len);
     g_launches++;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    *matches = c->h_ctr[0];
     return SIMBA_OK;
 }
 
@@ -3039,6 +3137,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
                            inputs + (size_t)idx[i - 1] * k))
                 return fail(SIMBA_EINVAL, "duplicate input tuple (pair %d)", idx[i]);
     }
+    CtxTrace tr;
     simba_options o{};
     if (opt)
         o = *opt;
@@ -3098,6 +3197,20 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     while (E > n)
         E >>= 1;
     c->E = E;
+    // Adaptive E (table_examples 0, searches of >= 2^30 candidates): the
+    // arena holds tables for up to Emax examples; after example 0's table is
+    // built its density decides whether examples 1.. get tables too, and the
+    // sparsest tabled example becomes example 0 -- all in this context.
+    unsigned __int128 cum = 0;
+    for (int z = 1; z <= max_size; ++z)
+        cum += c->rows[z][8];
+    const bool adapt = o.table_examples == 0 && n >= 2 && c->kernel == 0 && cum >= ((unsigned __int128)1 << 30);
+    int Emax = E;
+    if (adapt) {
+        Emax = 4;
+        while (Emax > n)
+            Emax >>= 1;
+    }
     // Value tables (per spec, memory independent of the search size):
     //   shared: example 0, every subtree of size <= R0 (the lane-varying digit)
     //   global: E examples, every subtree of size <= RG (left values, siblings)
@@ -3109,13 +3222,14 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     };
     // shared memory besides the value table: decoder tables, staged
     // examples, and per-warp levels + tile buffer for up to 16 warps
-    size_t lv = 0;
-    if (c->wbytes == 4)
-        lv = (E == 1) ? sizeof(WarpLevels<uint32_t, 1>) : (E == 2) ? sizeof(WarpLevels<uint32_t, 2>)
-                                                                 : sizeof(WarpLevels<uint32_t, 4>);
-    else
-        lv = (E == 1) ? sizeof(WarpLevels<uint64_t, 1>) : (E == 2) ? sizeof(WarpLevels<uint64_t, 2>)
-                                                                 : sizeof(WarpLevels<uint64_t, 4>);
+    auto lv_of = [&](int e) -> size_t {
+        if (c->wbytes == 4)
+            return (e == 1) ? sizeof(WarpLevels<uint32_t, 1>) : (e == 2) ? sizeof(WarpLevels<uint32_t, 2>)
+                                                                         : sizeof(WarpLevels<uint32_t, 4>);
+        return (e == 1) ? sizeof(WarpLevels<uint64_t, 1>) : (e == 2) ? sizeof(WarpLevels<uint64_t, 2>)
+                                                                     : sizeof(WarpLevels<uint64_t, 4>);
+    };
+    const size_t lv = lv_of(Emax);  // the column-size choice must hold for every E this context may take
     const uint64_t ex_b = ((uint64_t)n * (k + 1) * c->wbytes + 15) & ~15ull;
     // shared-memory budget of the value table for a CTA of `warps` warps
     auto table_cap = [&](int warps) -> uint64_t {
@@ -3178,7 +3292,6 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     c->r0_rows = SIMBA_R0_ROWS;
     if (const char *e = getenv("SIMBA_R0_ROWS"))
         c->r0_rows = strtoull(e, nullptr, 10);
-    c->y0 = outputs[0];
     if (const char *e = getenv("SIMBA_VT_DECODE"))
         c->value_tables_by_decode = atoi(e) != 0;
     if (const char *e = getenv("SIMBA_EX0_DENSE"))
@@ -3241,8 +3354,11 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     if (c->block_threads % 32 || c->block_threads < 32 || c->block_threads > SIMBA_UNIT_THREADS)
         return bail(fail(SIMBA_EINVAL, "block_threads must be a multiple of 32 in 32..%d", SIMBA_UNIT_THREADS));
     c->lvl_off = (uint32_t)(sizeof(Tabs) + c->tbl_bytes + (c->stage_examples ? c->ex_bytes : 0));
-    c->ps_off = (uint32_t)((c->lvl_off + lv * (c->block_threads / 32) + 15) & ~(size_t)15);
-    c->smem_unit = (int)(c->ps_off + sizeof(PlanShared));
+    auto set_layout = [&]() {  // shared-memory layout of unit_kernel<W, c->E>
+        c->ps_off = (uint32_t)((c->lvl_off + lv_of(c->E) * (c->block_threads / 32) + 15) & ~(size_t)15);
+        c->smem_unit = (int)(c->ps_off + sizeof(PlanShared));
+    };
+    set_layout();
     c->qcap = (uint32_t)(c->block_threads / 32 * kDescPerWarp);
     c->smem_direct = (int)(sizeof(Tabs) + (c->stage_examples ? c->ex_bytes : 0));
     // device state
@@ -3259,21 +3375,26 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     cudaError_t e;
     if ((e = cudaSetDevice(c->device)) != cudaSuccess)
         return cuda_bail(e, "cudaSetDevice");
-    if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess)
-        return cuda_bail(e, "cudaStreamCreate");
-    if ((e = cudaEventCreate(&c->ev0)) != cudaSuccess || (e = cudaEventCreate(&c->ev1)) != cudaSuccess)
-        return cuda_bail(e, "cudaEventCreate");
+    {
+        StreamSet ss;
+        if ((e = stream_get(c->device, &ss)) != cudaSuccess)
+            return cuda_bail(e, "cudaStreamCreate");
+        c->stream = ss.stream;
+        c->ev0 = ss.ev0;
+        c->ev1 = ss.ev1;
+    }
+    tr("stream + events");
     {
         // one device arena per context (tables, value tables, counters, tile
         // queue) and one pinned counter block, both from a process-wide pool:
         // cudaMalloc/cudaFree per synthesize call cost more than a small search
         size_t db = 0;
         if (c->wbytes == 4)
-            db = (E == 1) ? sizeof(TileDesc<uint32_t, 1>) : (E == 2) ? sizeof(TileDesc<uint32_t, 2>)
-                                                                     : sizeof(TileDesc<uint32_t, 4>);
+            db = (Emax == 1) ? sizeof(TileDesc<uint32_t, 1>) : (Emax == 2) ? sizeof(TileDesc<uint32_t, 2>)
+                                                                           : sizeof(TileDesc<uint32_t, 4>);
         else
-            db = (E == 1) ? sizeof(TileDesc<uint64_t, 1>) : (E == 2) ? sizeof(TileDesc<uint64_t, 2>)
-                                                                     : sizeof(TileDesc<uint64_t, 4>);
+            db = (Emax == 1) ? sizeof(TileDesc<uint64_t, 1>) : (Emax == 2) ? sizeof(TileDesc<uint64_t, 2>)
+                                                                           : sizeof(TileDesc<uint64_t, 4>);
         int sms = 0;
         if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess)
             return cuda_bail(e, "cudaDeviceGetAttribute");
@@ -3281,7 +3402,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         const size_t o_blob = up(sizeof(Tabs));
         const size_t o_gtbl = up(o_blob + (size_t)c->tbl_bytes + c->ex_bytes);
         // + kTblPad words: tiles read whole 256-column chunks past a row's end
-        const size_t o_ctr = up(o_gtbl + ((size_t)c->E * c->gtbl_len + kTblPad) * c->wbytes + 16);
+        const size_t o_ctr = up(o_gtbl + ((size_t)Emax * c->gtbl_len + kTblPad) * c->wbytes + 16);
         const size_t o_tok = up(o_ctr + sizeof(unsigned long long) * kCtrWords);
         const size_t o_stats = up(o_tok + sizeof(int32_t) * MAXS);
         const size_t o_queue = up(o_stats + sizeof(unsigned long long) * 2 * ST_N);
@@ -3310,6 +3431,7 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
         if (!c->h_ctr)
             return cuda_bail(e, "cudaMallocHost");
     }
+    tr("arena", c->stream);
     // examples as words W: inputs [n][k] then outputs [n]
     std::vector<unsigned char> ex(c->ex_bytes, 0);
     for (int i = 0; i < n * k; ++i) {
@@ -3335,89 +3457,68 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     if ((e = cudaMemcpyAsync(c->d_blob + c->tbl_bytes, ex.data(), c->ex_bytes, cudaMemcpyHostToDevice,
                              c->stream)) != cudaSuccess)
         return cuda_bail(e, "upload examples");
-    int rc = (c->wbytes == 4) ? build_value_tables<uint32_t>(c) : build_value_tables<uint64_t>(c);
+    int rc = (c->wbytes == 4) ? build_value_tables<uint32_t>(c, 0) : build_value_tables<uint64_t>(c, 0);
     if (rc)
         return bail(rc);
-    // (only where the search is large: below ~1e9 candidates the rebuild costs
-    // more than the hits it saves -- C2/C4 contexts 0.15 ms slower, same device time)
-    unsigned __int128 cum = 0;
-    for (int z = 1; z <= max_size; ++z)
-        cum += c->rows[z][8];
-    if (o.table_examples == 0 && n >= 2 && c->kernel == 0 && cum >= ((unsigned __int128)1 << 30)) {
-        simba_ctx *c4 = nullptr;
+    tr(c->E == 1 ? "uploads + value tables E=1" : "uploads + value tables E>1");
+    // (only where the search is large: below ~1e9 candidates the extra tables
+    // cost more than the hits they save -- C2/C4 contexts 0.15 ms slower)
+    if (adapt) {
+        unsigned long long m[4] = {0, 0, 0, 0};
         if (c->E == 1) {
-            // dense example 0: rebind with per-example value tables (E = 4)
-            unsigned long long matches = 0;
-            rc = (c->wbytes == 4) ? ex0_density<uint32_t>(c, &matches) : ex0_density<uint64_t>(c, &matches);
+            rc = (c->wbytes == 4) ? densities<uint32_t>(c, 1, outputs, m) : densities<uint64_t>(c, 1, outputs, m);
             if (rc)
                 return bail(rc);
-            if ((double)matches >= c->ex0_dense * (double)c->gtbl_len) {
-                simba_ctx_destroy(c);
-                simba_options o4 = o;
-                o4.table_examples = 4;
-                rc = simba_ctx_create(k, w, n, inputs, outputs, max_size, &o4, &c4);
-                if (rc)
-                    return rc;
-                c = nullptr;
-            }
-        } else {
-            // per-example tables chosen by the low-entropy rule: finish this
-            // context first (setup below), then check the primary example
-            c4 = nullptr;
-        }
-        if (c4 || c->E > 1) {
-            simba_ctx *ce = c4 ? c4 : c;
-            if (!c4) {
-                rc = (ce->wbytes == 4) ? setup_kernels<uint32_t>(ce) : setup_kernels<uint64_t>(ce);
+            tr("example-0 density");
+            if ((double)m[0] >= c->ex0_dense * (double)c->gtbl_len) {
+                // dense example 0: per-example value tables for examples 1..Emax-1
+                c->E = Emax;
+                rc = (c->wbytes == 4) ? build_value_tables<uint32_t>(c, 1) : build_value_tables<uint64_t>(c, 1);
                 if (rc)
                     return bail(rc);
-                l2_persist(ce);
-                int sms = 0;
-                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ce->device);
-                if (o.blocks_per_sm > 0) {
-                    ce->grid_unit = std::min(ce->grid_unit, sms * o.blocks_per_sm);
-                    ce->grid_direct = std::min(ce->grid_direct, sms * o.blocks_per_sm);
-                }
-                ce->grid_unit = std::min(ce->grid_unit, sms * 2);
+                tr("value tables of examples 1..E-1");
             }
+        }
+        if (c->E > 1) {
             // The tiles test one example; make it the sparsest of those with
             // tables (y0 = 0 on one example: 2% of all expressions match it,
             // and every match takes the slow hit path).  The order of the
             // examples does not change which candidates satisfy all of them.
+            rc = (c->wbytes == 4) ? densities<uint32_t>(c, c->E, outputs, m)
+                                  : densities<uint64_t>(c, c->E, outputs, m);
+            if (rc)
+                return bail(rc);
             int best = 0;
-            unsigned long long bm = ~0ull;
-            for (int e = 0; e < ce->E; ++e) {
-                unsigned long long m = 0;
-                rc = (ce->wbytes == 4) ? ex0_density<uint32_t>(ce, &m, e, outputs[e])
-                                       : ex0_density<uint64_t>(ce, &m, e, outputs[e]);
-                if (rc) {
-                    simba_ctx_destroy(ce);
-                    return rc;
-                }
-                if (m < bm) {
-                    bm = m;
-                    best = e;
-                }
+            for (int x = 1; x < c->E; ++x)
+                if (m[x] < m[best])
+                    best = x;
+            tr("per-example densities");
+            if (best != 0) {
+                // swap examples 0 and best: their rows of the staged examples
+                // and their value-table slices
+                const size_t wb = c->wbytes;
+                for (int j = 0; j < k; ++j)
+                    std::swap_ranges(&ex[(size_t)j * wb], &ex[(size_t)j * wb] + wb, &ex[((size_t)best * k + j) * wb]);
+                std::swap_ranges(&ex[(size_t)n * k * wb], &ex[(size_t)n * k * wb] + wb,
+                                 &ex[((size_t)n * k + best) * wb]);
+                if ((e = cudaMemcpyAsync(c->d_blob + c->tbl_bytes, ex.data(), c->ex_bytes, cudaMemcpyHostToDevice,
+                                         c->stream)) != cudaSuccess)
+                    return cuda_bail(e, "upload examples");
+                c->h2d_bytes += c->ex_bytes;
+                rc = (c->wbytes == 4) ? swap_slices<uint32_t>(c, best) : swap_slices<uint64_t>(c, best);
+                if (rc)
+                    return bail(rc);
+                tr("reorder examples", c->stream);
             }
-            if (best == 0) {
-                *out = ce;
-                return SIMBA_OK;
-            }
-            const int E = ce->E;
-            simba_ctx_destroy(ce);
-            std::vector<uint64_t> xin(inputs, inputs + (size_t)n * k), yout(outputs, outputs + n);
-            for (int j = 0; j < k; ++j)
-                std::swap(xin[j], xin[(size_t)best * k + j]);
-            std::swap(yout[0], yout[best]);
-            simba_options oe = o;
-            oe.table_examples = E;
-            return simba_ctx_create(k, w, n, xin.data(), yout.data(), max_size, &oe, out);
+            set_layout();
         }
     }
     rc = (c->wbytes == 4) ? setup_kernels<uint32_t>(c) : setup_kernels<uint64_t>(c);
     if (rc)
         return bail(rc);
+    tr("setup_kernels");
     l2_persist(c);
+    tr("l2_persist");
     {
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -3443,12 +3544,8 @@ void simba_ctx_destroy(simba_ctx *c)
         pool_put(c->device, c->arena, c->arena_bytes, false);
     if (c->h_ctr)
         pool_put(-1, c->h_ctr, sizeof(unsigned long long) * kCtrWords, true);
-    if (c->ev0)
-        cudaEventDestroy(c->ev0);
-    if (c->ev1)
-        cudaEventDestroy(c->ev1);
     if (c->stream)
-        cudaStreamDestroy(c->stream);
+        stream_put(StreamSet{c->device, c->stream, c->ev0, c->ev1});
     delete c;
 }
 
