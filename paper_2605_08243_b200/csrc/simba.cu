@@ -103,7 +103,7 @@ constexpr uint64_t kShuffleMult = 2246822507ULL;  // codec.py:29
 constexpr int kCtrWords = 10;  // ctr, best, count, visited, units[0..1], flags, units[3] (example-0 hits), planned,
                                // dropped (lowest rank of a run dropped by the time budget)
 constexpr int kLvlWords = 3 * (SIMBA_MAX_SIZE + 1);  // per-level count, visited, first rank
-constexpr uint64_t kFuseCands = 1ull << 26;          // synthesize: levels fused per launch up to this many candidates
+constexpr uint64_t kFuseCands = 1ull << 40;          // synthesize: levels fused per launch up to this many candidates
 constexpr uint64_t kSmemMax = 232448;  // opt-in dynamic shared memory per block (sm_100)
 #ifndef SIMBA_R0_ROWS
 #define SIMBA_R0_ROWS 16  // R0 + 1 needs the launch's first claims to span this many rows of T[R0+1]
@@ -1812,6 +1812,9 @@ __device__ __forceinline__ bool pool_pop(const KParams &p, uint64_t &a, uint64_t
 // kBigLaunch candidates (fewer, longer claims: fewer rows cut at claim
 // boundaries), twice that below (shorter tails when the launch is short)
 constexpr uint32_t kGuideBig = SIMBA_GUIDE;
+#ifndef SIMBA_SEARCH_DPW
+#define SIMBA_SEARCH_DPW 12  // descriptors per warp and phase of level-guided (fused) searches
+#endif
 #ifndef SIMBA_FUSED_GUIDE
 #define SIMBA_FUSED_GUIDE 2  // big multi-level launches (the C5 sweep): 19.75 -> 19.3 ms; a single level stays at 4
 #endif
@@ -1834,6 +1837,19 @@ __device__ __forceinline__ void run_piece(const KParams &p, uint64_t v, uint64_t
     vnext = pend;
 }
 
+// The chunk that ends the claims' guidance region from chunk v on: the end of
+// the launch, or with level guidance (one shard, chunk v at virtual rank
+// lo + v * chunk_len) the end of the level holding chunk v, so that a fused
+// search claims and plans each level as finely as a launch of its own and a
+// hit in a small level is not followed by large claims in the next.
+__device__ __forceinline__ uint64_t level_end(const KParams &p, uint64_t v)
+{
+    if (!(p.level_guide & 1) || v >= p.nvirt)
+        return p.nvirt;
+    const int s = level_of(p, p.lo + v * p.chunk_len);
+    return min(p.nvirt, ((uint64_t)p.vbase[s + 1] - p.lo + p.chunk_len - 1) / p.chunk_len);
+}
+
 __device__ __forceinline__ bool claim_run(const KParams &p, uint64_t t0, uint64_t &hint, Claim &cl)
 {
     const int lane = threadIdx.x & 31;
@@ -1849,7 +1865,7 @@ __device__ __forceinline__ bool claim_run(const KParams &p, uint64_t t0, uint64_
             cl.v0 = c;
             cl.v1 = min((uint64_t)(c + want), p.nvirt);
             const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-            hint = (p.nvirt - cl.v1) / (warps * p.guide);
+            hint = (level_end(p, cl.v1) - cl.v1) / (warps * p.guide);
             if (hint < 1)
                 hint = 1;
             // the time budget is polled between runs only and never masks a
@@ -1917,7 +1933,7 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
     const uint64_t t0 = globaltimer_ns();
     SweepStats ss{0, 0, 0};
     uint64_t vis = 0;
-    uint64_t hint = p.nvirt / ((uint64_t)gridDim.x * (blockDim.x >> 5) * p.guide);
+    uint64_t hint = level_end(p, 0) / ((uint64_t)gridDim.x * (blockDim.x >> 5) * p.guide);
     if (hint < 1)
         hint = 1;
     PlanShared *ps = plan_shared(p);
@@ -1967,7 +1983,12 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                 if (idx >= nq)
                     break;
                 SIMBA_WD("exec", idx, nq);
-                exec_desc<W, E>(p, st, q + ps->order[idx], lane, ss.count);
+                const TileDesc<W, E> *d = q + ps->order[idx];
+                // (searches: a tile whose first rank is above a recorded hit
+                // cannot hold the minimum -- planned before the hit was known)
+                if (early && p.vbase[d->s] + d->ubase + d->row0 * (uint64_t)d->R2 + d->clo > read_best(p))
+                    continue;
+                exec_desc<W, E>(p, st, d, lane, ss.count);
             }
             SIMBA_CYC_END(p, ST_W_EXEC, cwe);
             if (lane == 0)
@@ -1993,7 +2014,12 @@ __global__ void __launch_bounds__(SIMBA_UNIT_THREADS, 1) unit_kernel(const __gri
                 planned = *(volatile unsigned long long *)p.planned;
             planned = __shfl_sync(FULL, planned, 0);
             const uint64_t all = p.nvirt * p.chunk_len;
-            const uint64_t rem = all - min((uint64_t)planned, all);
+            uint64_t rem = all - min((uint64_t)planned, all);
+            if (p.level_guide & 2) {  // the level of the planning frontier (claims ascend)
+                const uint64_t f = min(p.lo + (uint64_t)planned, p.hi - 1);
+                const int fs = level_of(p, f);
+                rem = min(rem, (uint64_t)p.vbase[fs + 1] - f);
+            }
             od.phase_budget = p.phase_guide == 0
                                   ? ~0ull
                                   : max(p.desc_cands, rem / ((uint64_t)gridDim.x * (blockDim.x >> 5) * p.phase_guide));
@@ -2603,6 +2629,8 @@ struct simba_ctx {
     int fused_shards = 1;  // big shards take the one-GPU sweep's launch shape (SIMBA_FUSED_SHARDS=0: not)
     int absorb = 1;  // unary-topped right children of size R0+1 absorbed into P blocks (SIMBA_ABSORB=0: off)
     bool value_tables_by_decode = false;  // SIMBA_VT_DECODE=1: per-entry decode + eval (the cross-check)
+    int level_guide = 1;  // fused searches guided per level: claims 1, phase budgets 2, chunks 4 (SIMBA_LEVEL_GUIDE)
+    uint64_t fuse_cands = kFuseCands;  // synthesize: candidates per fused level group (SIMBA_FUSE_CANDS)
     double ex0_dense = 1e-4;  // example-0 match share of the value table from which E = 4 (SIMBA_EX0_DENSE)
     uint64_t last_super = 0;  // ranks per round-robin super-chunk of the last request
     uint64_t split_min = 0;  // pieces with at least this many ranks left split once claims run dry
@@ -2857,13 +2885,18 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
                        (unsigned long long)rq.shard, (unsigned long long)rq.nshards, rq.shuffled ? " shuffled" : "");
     const uint64_t range = rq.hi - rq.lo;
     const uint64_t warps = (uint64_t)(direct ? c->grid_direct : c->grid_unit) * (c->block_threads / 32);
+    const bool level_guide = c->level_guide && rq.mode == SIMBA_MODE_SEARCH && !rq.shuffled && rq.nshards == 1 &&
+                             s_lo < rq.size && !direct;
     // chunk = claim granularity; super-chunk = sharding unit (round robin)
     uint64_t chunk, spc;
     if (rq.chunk) {
         chunk = rq.chunk;
         spc = (rq.nshards > 1) ? 1 : (range + chunk - 1) / chunk;
     } else {
-        const uint64_t target = range / (warps * 64 * rq.nshards) + 1;
+        // (level-guided searches: chunks sized for the levels below the top one,
+        // so that each of them still spans many claims)
+        const uint64_t below = vbase[rq.size] > rq.lo ? std::min(vbase[rq.size], rq.hi) - rq.lo : range;
+        const uint64_t target = ((c->level_guide & 4) && level_guide ? below : range) / (warps * 64 * rq.nshards) + 1;
         chunk = 256;
         while (chunk < target && chunk < (1ull << SIMBA_CHUNK_LOG2))
             chunk <<= 1;
@@ -2943,6 +2976,10 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
     p.dpw_late = fused_big ? SIMBA_FUSED_DPW_LATE : 0;
     if (c->dpw_late_env >= 0)
         p.dpw_late = (uint32_t)std::min(c->dpw_late_env, kDescPerWarp);
+    if (level_guide) {  // short phases: a hit is recorded at the end of its phase (TTS s11 median 1.42 -> 0.93 ms)
+        p.dpw = std::min<uint32_t>(p.dpw, SIMBA_SEARCH_DPW);
+        p.dpw_late = 0;
+    }
     if (c->dpw_env)
         p.dpw = std::min<uint32_t>(c->dpw_env, kDescPerWarp);
     if (rq.nshards > 1 && c->shard_pg_env >= 0)
@@ -2951,6 +2988,7 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
         p.dpw = std::min<uint32_t>(c->shard_dpw_env, kDescPerWarp);
     p.s_lo = s_lo;
     p.s_hi = rq.size;
+    p.level_guide = level_guide ? c->level_guide : 0;
     p.vbase = c->d_lvl + kLvlWords;  // the level bases follow the per-level counters
     p.lvl = c->d_lvl;
     p.E = c->E;
@@ -3329,6 +3367,10 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     // late-splitting threshold; SIMBA_SPLIT_MIN (ranks) overrides it so that tests
     // can exercise the range pool on launches small enough for the CPU oracle
     c->split_min = kSplitMin;
+    if (const char *e = getenv("SIMBA_LEVEL_GUIDE"))
+        c->level_guide = atoi(e);
+    if (const char *e = getenv("SIMBA_FUSE_CANDS"))
+        c->fuse_cands = strtoull(e, nullptr, 10);
     if (const char *e = getenv("SIMBA_SPLIT_MIN"))
         c->split_min = std::max<uint64_t>(2, strtoull(e, nullptr, 10));
     {
@@ -3799,15 +3841,20 @@ int simba_synthesize(simba_ctx *c, int size_bound, int shuffled, double time_bud
     };
     if (!shuffled && c->kernel != 1) {
         // local order: consecutive levels are fused into one launch while they
-        // hold at most kFuseCands candidates (small levels cost launch latency,
-        // not work); a large level runs alone so that an early hit is not
-        // followed by claims far above it.  Each launch returns the minimum
-        // (size, rank) of its levels and per-level visited counts.
+        // hold at most kFuseCands candidates (2^40: every level of the C5
+        // suite).  The launch is level-guided (claims sized by the remaining
+        // ranks of their level, level_end) and skips tiles above a recorded
+        // hit, so an early hit is not followed by large claims in the next
+        // level, while no level pays a launch of its own: the small levels'
+        // tails overlap the next level's start (time to solve, C5 suite:
+        // medians 1.7 / 4.0 / 16.6 ms -> 0.9 / 2.9 / 14.4 ms at sizes
+        // 11 / 12 / 13).  Each launch returns the minimum (size, rank) of its
+        // levels and per-level visited counts.
         int s_lo = 1;
         while (s_lo <= size_bound) {
             int s_hi = s_lo;
             uint64_t acc = row_total(c, s_lo);
-            while (s_hi < size_bound && acc <= kFuseCands && row_total(c, s_hi + 1) <= kFuseCands - acc)
+            while (s_hi < size_bound && acc <= c->fuse_cands && row_total(c, s_hi + 1) <= c->fuse_cands - acc)
                 acc += row_total(c, ++s_hi);
             const auto t0 = clk::now();
             NvtxRange nvtx_lv("synthesize levels %d..%d", s_lo, s_hi);

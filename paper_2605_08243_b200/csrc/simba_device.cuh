@@ -80,6 +80,8 @@ struct KParams {
     uint64_t desc_cands;     // candidates per tile descriptor (at most)
     uint64_t split_min;      // late splitting: pieces with >= split_min ranks left
     uint64_t phase_guide;    // phase budget ~ remaining / (warps * phase_guide); 0: none
+    int level_guide;         // claims and phase budgets guided by the remaining ranks of the frontier's
+                             // level, not of the launch (fused single-shard searches)
     int mode;                // SIMBA_MODE_*
     int shuffled;
     uint64_t mask;
