@@ -1838,16 +1838,24 @@ __device__ __forceinline__ void run_piece(const KParams &p, uint64_t v, uint64_t
 }
 
 // The chunk that ends the claims' guidance region from chunk v on: the end of
-// the launch, or with level guidance (one shard, chunk v at virtual rank
-// lo + v * chunk_len) the end of the level holding chunk v, so that a fused
-// search claims and plans each level as finely as a launch of its own and a
-// hit in a small level is not followed by large claims in the next.
+// the launch, or with level guidance the first of this shard's chunks past
+// the level that holds chunk v, so that a fused search claims each level as
+// finely as a launch of its own and a hit in a small level is not followed by
+// large claims in the next.  (Chunk v of shard i lies in global super-chunk
+// i + (v / spc) * nshards, as in run_piece.)
 __device__ __forceinline__ uint64_t level_end(const KParams &p, uint64_t v)
 {
     if (!(p.level_guide & 1) || v >= p.nvirt)
         return p.nvirt;
-    const int s = level_of(p, p.lo + v * p.chunk_len);
-    return min(p.nvirt, ((uint64_t)p.vbase[s + 1] - p.lo + p.chunk_len - 1) / p.chunk_len);
+    const uint64_t sc = v / p.spc;
+    const uint64_t r = p.lo + ((p.shard + sc * p.nshards) * p.spc + (v - sc * p.spc)) * p.chunk_len;
+    if (r >= p.hi)
+        return p.nvirt;
+    const int s = level_of(p, r);
+    const uint64_t g = ((uint64_t)p.vbase[s + 1] - p.lo + p.chunk_len - 1) / p.chunk_len;  // first global chunk past it
+    const uint64_t gs = g / p.spc, d = gs - p.shard, k = d / p.nshards;
+    const uint64_t e = (d % p.nshards == 0) ? k * p.spc + (g - gs * p.spc) : (k + 1) * p.spc;
+    return min(p.nvirt, max(e, v + 1));
 }
 
 __device__ __forceinline__ bool claim_run(const KParams &p, uint64_t t0, uint64_t &hint, Claim &cl)
@@ -2885,8 +2893,8 @@ int run_req(simba_ctx *c, const Req &rq, simba_result *out)
                        (unsigned long long)rq.shard, (unsigned long long)rq.nshards, rq.shuffled ? " shuffled" : "");
     const uint64_t range = rq.hi - rq.lo;
     const uint64_t warps = (uint64_t)(direct ? c->grid_direct : c->grid_unit) * (c->block_threads / 32);
-    const bool level_guide = c->level_guide && rq.mode == SIMBA_MODE_SEARCH && !rq.shuffled && rq.nshards == 1 &&
-                             s_lo < rq.size && !direct;
+    const bool level_guide = c->level_guide && rq.mode == SIMBA_MODE_SEARCH && !rq.shuffled && s_lo < rq.size &&
+                             !direct;
     // chunk = claim granularity; super-chunk = sharding unit (round robin)
     uint64_t chunk, spc;
     if (rq.chunk) {
@@ -3550,6 +3558,8 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
                 rc = (c->wbytes == 4) ? swap_slices<uint32_t>(c, best) : swap_slices<uint64_t>(c, best);
                 if (rc)
                     return bail(rc);
+                if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess)  // a context is ready when created
+                    return cuda_bail(e, "reorder examples");
                 tr("reorder examples", c->stream);
             }
             set_layout();
@@ -3603,6 +3613,8 @@ int simba_xbest_create(int device, unsigned char *handle, simba_xbest **out)
     cudaIpcMemHandle_t h;
     cudaError_t e = cudaMemcpy(p, &none, sizeof(none), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
+        e = cudaStreamSynchronize(0);  // landed before the handle is shared (see simba_xbest_reset)
+    if (e == cudaSuccess)
         e = cudaIpcGetMemHandle(&h, p);
     if (e != cudaSuccess) {
         cudaFree(p);
@@ -3643,7 +3655,11 @@ int simba_xbest_reset(simba_xbest *x)
         return fail(SIMBA_EINVAL, "null shared minimum");
     CK(cudaSetDevice(x->device));
     const unsigned long long none = SIMBA_NO_RANK;
+    // a copy from pageable memory returns once the value is staged, before it
+    // lands; the other ranks launch right after this returns (barrier), so
+    // wait for it (8 ranks on one GPU read the previous search's minimum)
     CK(cudaMemcpy(x->word, &none, sizeof(none), cudaMemcpyHostToDevice));
+    CK(cudaStreamSynchronize(0));
     return SIMBA_OK;
 }
 

@@ -183,3 +183,50 @@ def test_shared_minimum_stops_a_shard_above_another_shards_hit():
     assert alone1.best_rank is not None and (alone1.size, alone1.best_rank) > want
     assert (r1.size, r1.best_rank) == want  # the pulled minimum
     assert r1.visited + (1 << 20) < alone1.visited, (r1.visited, alone1.visited)
+
+
+def _tts_rank_main(rank, world, port, specs, bound, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shared = parallel.shared_minimum(rank, world, device=0)
+        res = []
+        for pairs in specs:
+            dist.barrier()
+            spec = S.Specification(k=4, w=32, pairs=tuple(tuple(x) if isinstance(x, list) else x for x in pairs))
+            with DeviceContext(spec, bound, device=0) as ctx:
+                ctx.set_shared_minimum(shared)
+                size, first, _ = parallel.search_fused(parallel.device_levels(ctx), bound, rank, world, shared=shared)
+                ctx.set_shared_minimum(None)
+            res.append([size, first])
+        dist.barrier()
+        shared.close()
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_consecutive_searches_never_see_the_previous_minimum():
+    """Consecutive C5 time-to-solve targets on 8 processes sharing one minimum,
+    each right after a target with a smaller answer, two of them dense
+    (per-example tables, examples reordered at context creation).  The word's
+    reset must land before any rank launches: with a reset that returned once
+    its value was staged, 8 ranks on one GPU reported the previous target's
+    answer for s12_k4_i08 and s12_k4_i37."""
+    import torch.multiprocessing as mp
+    from conftest import load_golden
+
+    g = load_golden("c5")
+    recs = {r["id"]: r for recs in g["tts"].values() for r in recs}
+    order = ["s11_k4_i40", "s12_k4_i08", "s12_k4_i32", "s12_k4_i37", "s11_k4_i16", "s12_k4_i08"]
+    specs = [[(tuple(i), o) for i, o in recs[x]["spec"]["pairs"]] for x in order]
+    want = [[recs[x]["oracle"]["size"], recs[x]["oracle"]["rank"]] for x in order]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_tts_rank_main, args=(8, _free_port(), specs, 12, out), nprocs=8, join=True,
+                       start_method="spawn")
+    for rank in range(8):
+        assert out[rank] == want, rank
