@@ -229,3 +229,56 @@ def test_budget_never_reports_a_non_minimal_hit(mode):
             else:
                 assert out.status is S.Status.TIMED_OUT and out.expr is None
     assert S.Status.FOUND in seen
+
+
+# ------------------------------------------- per-example tables chosen at creation
+
+
+def _collapsed_spec(k, w, n, seed, target_size):
+    """Example 0 has all inputs equal (v, v, ..., v) -- most expressions
+    collapse onto a few values there, so example 0 is dense at its output --
+    the others are random; labelled by a uniform expression of target_size."""
+    from paper_2605_08243_b200 import codec, expr
+
+    rng = random.Random(seed)
+    e = codec.sample_uniform(target_size, S.build(k, target_size), rng)
+    v = rng.getrandbits(w) | (1 << (w - 1))
+    xs = [tuple([v] * k)]
+    while len(xs) < n:
+        x = tuple(rng.getrandbits(w) for _ in range(k))
+        if x not in xs:
+            xs.append(x)
+    return S.Specification(k=k, w=w, pairs=tuple((x, expr.evaluate(e, x, w)) for x in xs))
+
+
+@pytest.mark.parametrize("k,w,n,emax", [(3, 64, 3, 2), (3, 32, 5, 4)])
+def test_dense_example_zero_gets_tables_in_place_and_is_reordered(k, w, n, emax, monkeypatch):
+    """Searches of >= 2^30 candidates (k=3, sizes 1..12) measure example 0's
+    density after building its table; a dense example 0 makes the same
+    context add the other examples' tables (E = emax: n = 3 -> 2, n = 5 -> 4)
+    and swap the sparsest tabled example into place (their rows of the staged
+    examples and their table slices; 64-bit words too).  The answer is the
+    oracle's, as with tables for example 0 only (SIMBA_EX0_DENSE=2: never
+    dense)."""
+    spec = _collapsed_spec(k, w, n, 1000 + n, 7)
+    tab = O.OracleTable(k, 9)
+    want = None
+    for s in range(1, 10):
+        _, _, first, _ = O.scan_range(tab, k, w, [tuple(p) for p in spec.pairs], s, 0, tab.total(s), 0, tab.total(s),
+                                      threads=O.cpu_count())
+        if first is not None:
+            want = (s, first)
+            break
+    assert want is not None
+    table = S.build(k, 12)
+    with DeviceContext(spec, 12) as ctx:
+        assert ctx.info()["table_examples"] == emax
+        r, _ = ctx.run_levels(1, 12, mode="search")
+        assert (r.size, r.best_rank) == want
+    out = S.synthesize(spec, table, S.EngineConfig(size_bound=12))
+    assert (out.size, out.rank) == want
+    monkeypatch.setenv("SIMBA_EX0_DENSE", "2")
+    with DeviceContext(spec, 12) as ctx:
+        assert ctx.info()["table_examples"] == 1
+        r, _ = ctx.run_levels(1, 12, mode="search")
+        assert (r.size, r.best_rank) == want
