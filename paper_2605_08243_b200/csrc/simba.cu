@@ -2301,20 +2301,15 @@ __global__ void ex0_density_kernel(const W *g, uint32_t len, W y0, W mask, unsig
         atomicAdd(out, (unsigned long long)cnt);
 }
 
-// Value table level `sz`, built bottom-up from the levels below it: entry r of
-// size sz is its top operator applied to one or two table entries of smaller
-// sizes -- the first step of decode_into (codec.py:108-130) and one operation
-// of eval_tokens, in the same full word width (so the values equal
+// Entry r of size sz of example e's value table, built bottom-up from the
+// levels below it: its top operator applied to one or two table entries of
+// smaller sizes -- the first step of decode_into (codec.py:108-130) and one
+// operation of eval_tokens, in the same full word width (so the values equal
 // value_table_kernel's decode + eval_rpn per entry, at a fraction of the work).
 template <class W>
-__global__ void value_level_kernel(const Tabs *tabs, const W *X, int k, int sz, int e0, int E, uint32_t tbl_len,
-                                   W *out)
+__device__ __forceinline__ W value_level_entry(const Tabs *tabs, const W *X, int k, int sz, uint32_t e, uint32_t r,
+                                               uint32_t tbl_len, W *out)
 {
-    const uint32_t n = (uint32_t)tabs->T[sz];
-    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (uint32_t)(E - e0) * n)
-        return;
-    const uint32_t e = e0 + idx / n, r = idx % n;
     W *g = out + (size_t)e * tbl_len;
     W v;
     if (sz == 1) {
@@ -2335,7 +2330,33 @@ __global__ void value_level_kernel(const Tabs *tabs, const W *X, int k, int sz, 
         }
     }
     g[tabs->toff[sz] + r] = v;
+    return v;
 }
+
+// Value table level `sz` of examples e0..E-1 (value_level_entry per entry);
+// with `dens`, also the entries equal to each example's output (the density
+// that chooses E), so no separate pass over the table is needed.
+template <class W>
+__global__ void value_level_kernel(const Tabs *tabs, const W *X, int k, int sz, int e0, int E, uint32_t tbl_len,
+                                   W *out, const W *ys, W mask, unsigned long long *dens)
+{
+    const uint32_t n = (uint32_t)tabs->T[sz];
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = idx < (uint32_t)(E - e0) * n;
+    const uint32_t e = valid ? e0 + idx / n : (uint32_t)e0, r = valid ? idx % n : 0u;
+    if (dens) {  // entries equal to example e's output, counted as they are made (ex0_density_kernel's count)
+        const W v = valid ? value_level_entry<W>(tabs, X, k, sz, e, r, tbl_len, out) : (W)0;
+        for (int q = e0; q < E; ++q) {
+            const unsigned int b = __ballot_sync(FULL, valid && e == (uint32_t)q && ((v ^ ys[q]) & mask) == 0);
+            if ((threadIdx.x & 31) == 0 && b)
+                atomicAdd(dens + q, (unsigned long long)__popc(b));
+        }
+        return;
+    }
+    if (valid)
+        value_level_entry<W>(tabs, X, k, sz, e, r, tbl_len, out);
+}
+
 
 template <class W>
 __global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int RG, int e0, int E, uint32_t tbl_len,
@@ -2705,11 +2726,16 @@ int setup_kernels(simba_ctx *c)
 // Value tables of examples e0..E-1 (0: all; 1: the per-example tables added
 // when example 0 proves dense, next to its own).
 template <class W>
-int build_value_tables(simba_ctx *c, int e0)
+int build_value_tables(simba_ctx *c, int e0, bool density = false)
 {
     const int bt = 256;
     const W *X = reinterpret_cast<const W *>(c->d_blob + c->tbl_bytes);
     W *G = reinterpret_cast<W *>(c->d_gtbl);
+    // (densities: entries equal to example e's output land in d_ctr[e] and
+    // h_ctr[e]; the decode cross-check path counts them in a pass of its own)
+    unsigned long long *dens = (density && !c->value_tables_by_decode) ? c->d_ctr : nullptr;
+    if (dens)
+        CK(cudaMemsetAsync(dens, 0, sizeof(unsigned long long) * 4, c->stream));
     if (c->value_tables_by_decode) {  // reference-exact decode + eval per entry (SIMBA_VT_DECODE=1; tests)
         const uint32_t total = (uint32_t)(c->E - e0) * c->gtbl_len;
         value_table_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(c->d_tabs, X, c->k, c->RG, e0, c->E,
@@ -2719,12 +2745,14 @@ int build_value_tables(simba_ctx *c, int e0)
     } else {  // bottom-up, one launch per size (each level reads only the ones below)
         for (int sz = 1; sz <= c->RG; ++sz) {
             const uint32_t total = (uint32_t)(c->E - e0) * (uint32_t)c->h_tabs.T[sz];
-            value_level_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(c->d_tabs, X, c->k, sz, e0, c->E,
-                                                                              c->gtbl_len, G);
+            value_level_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(
+                c->d_tabs, X, c->k, sz, e0, c->E, c->gtbl_len, G, X + (size_t)c->n * c->k, (W)c->mask, dens);
             g_launches++;
             CK(cudaGetLastError());
         }
     }
+    if (dens)
+        CK(cudaMemcpyAsync(c->h_ctr, dens, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return SIMBA_OK;
 }
@@ -3507,37 +3535,44 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     if ((e = cudaMemcpyAsync(c->d_blob + c->tbl_bytes, ex.data(), c->ex_bytes, cudaMemcpyHostToDevice,
                              c->stream)) != cudaSuccess)
         return cuda_bail(e, "upload examples");
-    int rc = (c->wbytes == 4) ? build_value_tables<uint32_t>(c, 0) : build_value_tables<uint64_t>(c, 0);
+    int rc = (c->wbytes == 4) ? build_value_tables<uint32_t>(c, 0, adapt) : build_value_tables<uint64_t>(c, 0, adapt);
     if (rc)
         return bail(rc);
     tr(c->E == 1 ? "uploads + value tables E=1" : "uploads + value tables E>1");
     // (only where the search is large: below ~1e9 candidates the extra tables
     // cost more than the hits they save -- C2/C4 contexts 0.15 ms slower)
     if (adapt) {
+        // per-example densities (entries equal to the example's output),
+        // counted while the tables were built
         unsigned long long m[4] = {0, 0, 0, 0};
-        if (c->E == 1) {
-            rc = (c->wbytes == 4) ? densities<uint32_t>(c, 1, outputs, m) : densities<uint64_t>(c, 1, outputs, m);
-            if (rc)
-                return bail(rc);
-            tr("example-0 density");
-            if ((double)m[0] >= c->ex0_dense * (double)c->gtbl_len) {
-                // dense example 0: per-example value tables for examples 1..Emax-1
-                c->E = Emax;
-                rc = (c->wbytes == 4) ? build_value_tables<uint32_t>(c, 1) : build_value_tables<uint64_t>(c, 1);
-                if (rc)
-                    return bail(rc);
-                tr("value tables of examples 1..E-1");
+        auto take = [&](int e_lo) -> int {
+            if (c->value_tables_by_decode) {  // the decode cross-check counts in a pass of its own
+                unsigned long long t4[4] = {0, 0, 0, 0};
+                int r2 = (c->wbytes == 4) ? densities<uint32_t>(c, c->E, outputs, t4)
+                                          : densities<uint64_t>(c, c->E, outputs, t4);
+                for (int x = e_lo; x < c->E; ++x)
+                    m[x] = t4[x];
+                return r2;
             }
+            for (int x = e_lo; x < c->E; ++x)
+                m[x] = c->h_ctr[x];
+            return SIMBA_OK;
+        };
+        if ((rc = take(0)))
+            return bail(rc);
+        if (c->E == 1 && (double)m[0] >= c->ex0_dense * (double)c->gtbl_len) {
+            // dense example 0: per-example value tables for examples 1..Emax-1
+            c->E = Emax;
+            rc = (c->wbytes == 4) ? build_value_tables<uint32_t>(c, 1, true) : build_value_tables<uint64_t>(c, 1, true);
+            if (rc || (rc = take(1)))
+                return bail(rc);
+            tr("value tables of examples 1..E-1");
         }
         if (c->E > 1) {
             // The tiles test one example; make it the sparsest of those with
             // tables (y0 = 0 on one example: 2% of all expressions match it,
             // and every match takes the slow hit path).  The order of the
             // examples does not change which candidates satisfy all of them.
-            rc = (c->wbytes == 4) ? densities<uint32_t>(c, c->E, outputs, m)
-                                  : densities<uint64_t>(c, c->E, outputs, m);
-            if (rc)
-                return bail(rc);
             int best = 0;
             for (int x = 1; x < c->E; ++x)
                 if (m[x] < m[best])
