@@ -3535,10 +3535,11 @@ int simba_ctx_create(int k, int w, int n, const uint64_t *inputs, const uint64_t
     if ((e = cudaMemcpyAsync(c->d_blob + c->tbl_bytes, ex.data(), c->ex_bytes, cudaMemcpyHostToDevice,
                              c->stream)) != cudaSuccess)
         return cuda_bail(e, "upload examples");
+    tr("uploads", c->stream);
     int rc = (c->wbytes == 4) ? build_value_tables<uint32_t>(c, 0, adapt) : build_value_tables<uint64_t>(c, 0, adapt);
     if (rc)
         return bail(rc);
-    tr(c->E == 1 ? "uploads + value tables E=1" : "uploads + value tables E>1");
+    tr(c->E == 1 ? "value tables E=1" : "value tables E>1");
     // (only where the search is large: below ~1e9 candidates the extra tables
     // cost more than the hits they save -- C2/C4 contexts 0.15 ms slower)
     if (adapt) {
