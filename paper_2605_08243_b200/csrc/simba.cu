@@ -2301,62 +2301,121 @@ __global__ void ex0_density_kernel(const W *g, uint32_t len, W y0, W mask, unsig
         atomicAdd(out, (unsigned long long)cnt);
 }
 
-// Entry r of size sz of example e's value table, built bottom-up from the
-// levels below it: its top operator applied to one or two table entries of
+// Value table level `sz` of examples e0..E-1, built bottom-up from the levels
+// below it: entry r is its top operator applied to one or two entries of
 // smaller sizes -- the first step of decode_into (codec.py:108-130) and one
 // operation of eval_tokens, in the same full word width (so the values equal
 // value_table_kernel's decode + eval_rpn per entry, at a fraction of the work).
+// Each warp takes VL_STEPS consecutive groups of 32 entries; a lane finds its
+// entry's operator block, split and child ranks once (find_slot, find_split,
+// one division) and then steps them by 32 like an odometer, searching again
+// only when it leaves the block (the per-entry search and division made the
+// build instruction-bound).  The search reads the level's prefix sums from
+// shared memory (from global memory its chain of dependent loads cost 10-16
+// us per launch even for the 4-entry levels).  With `dens`, the entries equal
+// to each example's output are counted as they are made (the density that
+// chooses E).
+constexpr int VL_STEPS = 16;
+
+struct LevelTabs {
+    unsigned long long slot[8], split[MAXS];
+    uint32_t T[MAXS + 1], toff[MAXS + 1];
+};
+
 template <class W>
-__device__ __forceinline__ W value_level_entry(const Tabs *tabs, const W *X, int k, int sz, uint32_t e, uint32_t r,
-                                               uint32_t tbl_len, W *out)
+__global__ void __launch_bounds__(256) value_level_kernel(const Tabs *tabs, const W *X, int k, int sz, int e0, int E,
+                                                          uint32_t tbl_len, W *out, const W *ys, W mask,
+                                                          unsigned long long *dens)
 {
-    W *g = out + (size_t)e * tbl_len;
-    W v;
-    if (sz == 1) {
-        v = X[(size_t)e * k + r];
-    } else {
-        uint64_t rr = r;
-        const int op = find_slot(tabs, sz, rr);
-        if (op == OP_NOT || op == OP_NEG) {
-            const W a = g[tabs->toff[sz - 1] + (uint32_t)rr];
-            v = (op == OP_NOT) ? (W)~a : (W)((W)0 - a);
-        } else {
-            const int j = find_split(tabs, sz, rr);
-            const int rsz = sz - 1 - j;
-            const uint64_t q = rr / tabs->T[rsz];
-            const W a = g[tabs->toff[j] + (uint32_t)q];
-            const W b = g[tabs->toff[rsz] + (uint32_t)(rr - q * tabs->T[rsz])];
-            v = apply_bin<W>(op, a, b);
+    __shared__ LevelTabs lt;
+    if (threadIdx.x <= MAXS) {  // one parallel load per value
+        const int i = threadIdx.x;
+        if (i < 8)
+            lt.slot[i] = tabs->slot_cum[sz][i];
+        if (i < MAXS)
+            lt.split[i] = tabs->split_cum[sz][i];
+        lt.T[i] = (uint32_t)min(tabs->T[i], (uint64_t)0xffffffffu);
+        lt.toff[i] = tabs->toff[i];
+    }
+    __syncthreads();
+    const uint32_t n = lt.T[sz];
+    const uint32_t total = (uint32_t)(E - e0) * n;
+    const uint32_t wbase = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32u * VL_STEPS);
+    uint32_t idx = wbase + (threadIdx.x & 31);
+    uint32_t e = (uint32_t)e0 + idx / n, r = idx % n;
+    const uint32_t toff_s = lt.toff[sz];
+    // odometer state of the current block: valid for r < end
+    int op = -1;
+    uint32_t end = 0, offa = 0, offb = 0, rem = 0, Tr = 1;
+    for (int m = 0; m < VL_STEPS; ++m, idx += 32) {
+        const bool valid = idx < total;
+        W v = (W)0;
+        if (valid) {
+            const W *g = out + (size_t)e * tbl_len;
+            if (sz == 1) {
+                v = X[(size_t)e * k + r];
+            } else {
+                if (op < 0 || r >= end) {  // find_slot / find_split on the staged sums
+                    uint32_t rr = r;
+                    op = 0;
+                    while (rr >= lt.slot[op])
+                        ++op;
+                    if (op)
+                        rr -= (uint32_t)lt.slot[op - 1];
+                    if (op == OP_NOT || op == OP_NEG) {
+                        end = r - rr + lt.T[sz - 1];
+                        offa = lt.toff[sz - 1] + rr;
+                    } else {
+                        int j = 1;
+                        while (rr >= lt.split[j])
+                            ++j;
+                        rr -= (uint32_t)lt.split[j - 1];
+                        const int rsz = sz - 1 - j;
+                        Tr = lt.T[rsz];
+                        const uint32_t q = rr / Tr;
+                        rem = rr - q * Tr;
+                        offa = lt.toff[j] + q;
+                        offb = lt.toff[rsz];
+                        end = r - rr + lt.T[j] * Tr;
+                    }
+                }
+                const W a = g[offa];
+                if (op == OP_NOT)
+                    v = (W)~a;
+                else if (op == OP_NEG)
+                    v = (W)((W)0 - a);
+                else
+                    v = apply_bin<W>(op, a, g[offb + rem]);
+            }
+            out[(size_t)e * tbl_len + toff_s + r] = v;
+        }
+        if (dens) {
+            for (int q = e0; q < E; ++q) {
+                const unsigned int b = __ballot_sync(FULL, valid && e == (uint32_t)q && ((v ^ ys[q]) & mask) == 0);
+                if ((threadIdx.x & 31) == 0 && b)
+                    atomicAdd(dens + q, (unsigned long long)__popc(b));
+            }
+        }
+        // next entry of this lane: 32 ranks on
+        r += 32;
+        if (op >= 0 && r < end) {
+            if (op == OP_NOT || op == OP_NEG) {
+                offa += 32;
+            } else {
+                rem += 32;
+                while (rem >= Tr) {
+                    rem -= Tr;
+                    ++offa;
+                }
+            }
+        }
+        while (r >= n) {  // into the next example's table: search again
+            r -= n;
+            ++e;
+            op = -1;
         }
     }
-    g[tabs->toff[sz] + r] = v;
-    return v;
 }
-
-// Value table level `sz` of examples e0..E-1 (value_level_entry per entry);
-// with `dens`, also the entries equal to each example's output (the density
-// that chooses E), so no separate pass over the table is needed.
-template <class W>
-__global__ void value_level_kernel(const Tabs *tabs, const W *X, int k, int sz, int e0, int E, uint32_t tbl_len,
-                                   W *out, const W *ys, W mask, unsigned long long *dens)
-{
-    const uint32_t n = (uint32_t)tabs->T[sz];
-    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = idx < (uint32_t)(E - e0) * n;
-    const uint32_t e = valid ? e0 + idx / n : (uint32_t)e0, r = valid ? idx % n : 0u;
-    if (dens) {  // entries equal to example e's output, counted as they are made (ex0_density_kernel's count)
-        const W v = valid ? value_level_entry<W>(tabs, X, k, sz, e, r, tbl_len, out) : (W)0;
-        for (int q = e0; q < E; ++q) {
-            const unsigned int b = __ballot_sync(FULL, valid && e == (uint32_t)q && ((v ^ ys[q]) & mask) == 0);
-            if ((threadIdx.x & 31) == 0 && b)
-                atomicAdd(dens + q, (unsigned long long)__popc(b));
-        }
-        return;
-    }
-    if (valid)
-        value_level_entry<W>(tabs, X, k, sz, e, r, tbl_len, out);
-}
-
 
 template <class W>
 __global__ void value_table_kernel(const Tabs *tabs, const W *X, int k, int RG, int e0, int E, uint32_t tbl_len,
@@ -2745,7 +2804,8 @@ int build_value_tables(simba_ctx *c, int e0, bool density = false)
     } else {  // bottom-up, one launch per size (each level reads only the ones below)
         for (int sz = 1; sz <= c->RG; ++sz) {
             const uint32_t total = (uint32_t)(c->E - e0) * (uint32_t)c->h_tabs.T[sz];
-            value_level_kernel<W><<<(total + bt - 1) / bt, bt, 0, c->stream>>>(
+            const uint32_t per_block = (uint32_t)bt * VL_STEPS;  // entries per block
+            value_level_kernel<W><<<(total + per_block - 1) / per_block, bt, 0, c->stream>>>(
                 c->d_tabs, X, c->k, sz, e0, c->E, c->gtbl_len, G, X + (size_t)c->n * c->k, (W)c->mask, dens);
             g_launches++;
             CK(cudaGetLastError());
