@@ -260,7 +260,7 @@ def test_dense_example_zero_gets_tables_in_place_and_is_reordered(k, w, n, emax,
     examples and their table slices; 64-bit words too).  The answer is the
     oracle's, as with tables for example 0 only (SIMBA_EX0_DENSE=2: never
     dense)."""
-    spec = _collapsed_spec(k, w, n, 1000 + n, 7)
+    spec = _collapsed_spec(k, w, n, 2001, 7)  # minimal answer at size 7 (seed 1003: size 2)
     tab = O.OracleTable(k, 9)
     want = None
     for s in range(1, 10):
